@@ -1,0 +1,132 @@
+/*
+ * kvswap.h — C ABI of the B200 KV-swap data plane (libkvswap.so).
+ *
+ * The reference (kvswitch, FastSwitch arXiv 2411.18424) has no FFI: its swap
+ * "data plane" is the timing model inside SwapManager.dispatch
+ * (pkg/src/kvswitch/swap.py:181-232) driven by TransferOp lists
+ * (pkg/src/kvswitch/cpu_store.py:73-92).  Every entry point below is what a
+ * maintainer binds *underneath* that method (see INTEGRATION.md for the
+ * ctypes stub); each one names the reference interface it replaces.
+ *
+ * Conventions
+ *  - All functions return int: 0 = KVS_OK, > 0 = a cudaError_t, < 0 = a
+ *    KVS_ERR_* library code.  kvs_error_string() renders either kind.
+ *  - No torch / CUDA types in signatures: streams are passed as uint64_t
+ *    (the value of cudaStream_t / torch.cuda.Stream.cuda_stream), device and
+ *    host addresses as plain pointers / uint64_t.
+ *  - Ops are the reference's TransferOp triples, flattened as int32
+ *    [blocks, gpu_start, cpu_start] × n_ops (cpu_store.py:73-79).
+ *  - Direction: KVS_DIR_OUT = swap-out (HBM -> pinned host, "out" in
+ *    SwapPlan.direction), KVS_DIR_IN = swap-in (host -> HBM, "in").
+ *
+ * Geometry (one handle per GPU / TP rank):
+ *  The rank's paged KV cache is `num_planes` device "planes".  A plane is one
+ *  contiguous array of per-block chunks: block b of plane p lives at
+ *  plane_ptrs[p] + b * plane_block_stride and is plane_chunk_bytes long.
+ *  FlashInfer/vLLM-v1 per-layer [num_blocks, 2, 16, H, d] tensors are one plane
+ *  per layer; split-K/V [2, num_blocks, ...] layouts are two planes per layer.
+ *  The host pool is block-major: host block c is one contiguous extent of
+ *  num_planes * plane_chunk_bytes bytes (plane p at offset p * chunk), so a
+ *  host block group (cpu_store.py:134, a BlockGroupPool over host blocks) is
+ *  one contiguous byte range and swap-out writes long sequential PCIe runs.
+ */
+#ifndef KVSWAP_H_
+#define KVSWAP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVS_ABI_VERSION 1
+
+#define KVS_OK 0
+#define KVS_ERR_INVALID (-1)   /* bad argument (reference: ValueError)              */
+#define KVS_ERR_RANGE (-2)     /* op outside a pool (reference: PoolError/IndexError) */
+#define KVS_ERR_ALIGN (-3)     /* pointer/size not 16-byte aligned                   */
+#define KVS_ERR_NOMEM (-4)     /* host allocation / pinning failed                   */
+#define KVS_ERR_UNSUPPORTED (-5) /* driver lacks a required feature                  */
+
+#define KVS_DIR_OUT 0
+#define KVS_DIR_IN 1
+
+/* kvs_memcpy_baseline modes (copy-engine comparators). */
+#define KVS_BASE_PER_BLOCK 0 /* vLLM: one cudaMemcpyAsync per (plane, block)      */
+#define KVS_BASE_PER_RUN 1   /* block groups on the CE: one cudaMemcpy2DAsync per (plane, op) */
+#define KVS_BASE_BATCH 2     /* one cudaMemcpyBatchAsync per plan (CUDA >= 12.8)  */
+
+/* kvs_host_alloc flags */
+#define KVS_HOST_DEFAULT 0
+#define KVS_HOST_REGISTER 1 /* mmap + (optional) mbind + cudaHostRegister instead of cudaHostAlloc */
+
+typedef struct KvsGeometry {
+  int32_t num_planes;         /* P >= 1                                        */
+  int32_t reserved;           /* must be 0                                     */
+  int64_t plane_chunk_bytes;  /* bytes of one block in one plane, % 16 == 0    */
+  int64_t plane_block_stride; /* bytes between blocks in a plane, >= chunk, %16 */
+} KvsGeometry;
+
+typedef struct KvsHandle KvsHandle;
+
+/* ABI version of the loaded library (== KVS_ABI_VERSION). */
+int kvs_abi_version(void);
+
+/* Human-readable text for any return code. Never NULL. */
+const char* kvs_error_string(int code);
+
+/* Create a data-plane handle for one device (one TP rank).
+ * Replaces: the bytes_per_block-only geometry SwapManager keeps
+ * (swap.py:141-145, core.py:27-38); it borrows every pointer, owns none.
+ * plane_ptrs: host array of num_planes device addresses (16-B aligned).
+ * host_base: device-usable address of the mapped pinned host pool
+ *            (num_cpu_blocks * num_planes * chunk bytes). */
+int kvs_create(int device, const KvsGeometry* geo, const uint64_t* plane_ptrs,
+               void* host_base, int64_t num_gpu_blocks, int64_t num_cpu_blocks,
+               KvsHandle** out);
+
+int kvs_destroy(KvsHandle* h);
+
+/* Launch shape of the gather/scatter kernel for one direction.
+ * ctas: persistent CTAs (0 = library default); threads: per CTA (multiple of 32,
+ * 0 = default).  Bounded footprint keeps decode SMs free (swap.py:256-268
+ * yield analogue). */
+int kvs_set_launch(KvsHandle* h, int dir, int ctas, int threads);
+
+/* Queue one SwapPlan's bytes on `stream` — asynchronous, no host blocking,
+ * no allocation.  Replaces the modeled copy-engine timeline of
+ * SwapManager.dispatch (swap.py:193-205, costmodel.py:29-31).
+ * ops: n_ops x [blocks, gpu_start, cpu_start] (TransferOp, cpu_store.py:73-79).
+ * done_flag (optional, may be NULL): device-visible uint32 (device memory or
+ * mapped host) that receives `seq` with system-scope release once every byte
+ * of this call has landed; pair with kvs_wait_flag for cross-stream waits
+ * (reference: OpRecord.exec_done / not_before, swap.py:36-42, 186). */
+int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
+             uint64_t stream, uint32_t* done_flag, uint32_t seq);
+
+/* Make `stream` wait until *flag >= value (cuStreamWaitValue32 GEQ).
+ * Replaces: not_before / conflict dependencies (engine.py:712-719,
+ * swap.py:236-252) as a device-side wait instead of a modeled timestamp. */
+int kvs_wait_flag(uint64_t stream, const uint32_t* flag, uint32_t value);
+
+/* Number of kernels this handle has launched (gpu_launches evidence). */
+int64_t kvs_launch_count(const KvsHandle* h);
+
+/* Copy-engine comparators for the same plan (vLLM per-block, per-run 2D,
+ * cudaMemcpyBatchAsync).  Reference: split_single (swap.py:170-179) is the
+ * per-block mode; block groups (alloc.py) are the per-run mode. */
+int kvs_memcpy_baseline(KvsHandle* h, int dir, int mode, const int32_t* ops,
+                        int32_t n_ops, uint64_t stream);
+
+/* Pinned, device-mapped host pool (CpuStore's backing bytes,
+ * cpu_store.py:126-141).  numa_node < 0: no binding.  *dev receives the
+ * device-usable address (== *host under UVA). */
+int kvs_host_alloc(size_t bytes, int numa_node, int flags, void** host, void** dev);
+int kvs_host_free(void* host);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KVSWAP_H_ */

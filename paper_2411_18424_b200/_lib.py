@@ -1,0 +1,149 @@
+"""ctypes binding of libkvswap.so (include/kvswap.h).
+
+This is the product path: there is no CPU fallback.  If the shared library
+is missing or fails to load, every data-plane call raises NativeLibraryError.
+Return codes map onto the reference's exception vocabulary: bad arguments
+raise ValueError (as kvswitch does, e.g. alloc.py:233-234), ops outside a pool
+raise IndexError, CUDA failures raise KvSwapCudaError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+from typing import Optional
+
+LIB_PATH = Path(__file__).resolve().parent / "libkvswap.so"
+
+KVS_OK = 0
+KVS_ERR_INVALID = -1
+KVS_ERR_RANGE = -2
+KVS_ERR_ALIGN = -3
+KVS_ERR_NOMEM = -4
+KVS_ERR_UNSUPPORTED = -5
+
+KVS_DIR_OUT = 0
+KVS_DIR_IN = 1
+
+KVS_BASE_PER_BLOCK = 0
+KVS_BASE_PER_RUN = 1
+KVS_BASE_BATCH = 2
+
+KVS_HOST_DEFAULT = 0
+KVS_HOST_REGISTER = 1
+
+# Every symbol include/kvswap.h declares; tests assert all are exported.
+EXPORTED_SYMBOLS = (
+    "kvs_abi_version",
+    "kvs_error_string",
+    "kvs_create",
+    "kvs_destroy",
+    "kvs_set_launch",
+    "kvs_swap",
+    "kvs_wait_flag",
+    "kvs_launch_count",
+    "kvs_memcpy_baseline",
+    "kvs_host_alloc",
+    "kvs_host_free",
+)
+
+DIRECTIONS = {"out": KVS_DIR_OUT, "in": KVS_DIR_IN}
+
+
+class NativeLibraryError(RuntimeError):
+    """libkvswap.so is missing or unusable; the data plane has no fallback."""
+
+
+class KvSwapCudaError(RuntimeError):
+    """A CUDA runtime/driver call inside libkvswap failed."""
+
+
+class KvsGeometry(ctypes.Structure):
+    _fields_ = [
+        ("num_planes", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("plane_chunk_bytes", ctypes.c_int64),
+        ("plane_block_stride", ctypes.c_int64),
+    ]
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def _declare(lib: ctypes.CDLL) -> None:
+    c = ctypes
+    lib.kvs_abi_version.restype = c.c_int
+    lib.kvs_abi_version.argtypes = []
+    lib.kvs_error_string.restype = c.c_char_p
+    lib.kvs_error_string.argtypes = [c.c_int]
+    lib.kvs_create.restype = c.c_int
+    lib.kvs_create.argtypes = [
+        c.c_int, c.POINTER(KvsGeometry), c.POINTER(c.c_uint64), c.c_void_p,
+        c.c_int64, c.c_int64, c.POINTER(c.c_void_p),
+    ]
+    lib.kvs_destroy.restype = c.c_int
+    lib.kvs_destroy.argtypes = [c.c_void_p]
+    lib.kvs_set_launch.restype = c.c_int
+    lib.kvs_set_launch.argtypes = [c.c_void_p, c.c_int, c.c_int, c.c_int]
+    lib.kvs_swap.restype = c.c_int
+    lib.kvs_swap.argtypes = [
+        c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64, c.c_void_p, c.c_uint32,
+    ]
+    lib.kvs_wait_flag.restype = c.c_int
+    lib.kvs_wait_flag.argtypes = [c.c_uint64, c.c_void_p, c.c_uint32]
+    lib.kvs_launch_count.restype = c.c_int64
+    lib.kvs_launch_count.argtypes = [c.c_void_p]
+    lib.kvs_memcpy_baseline.restype = c.c_int
+    lib.kvs_memcpy_baseline.argtypes = [
+        c.c_void_p, c.c_int, c.c_int, c.c_void_p, c.c_int32, c.c_uint64,
+    ]
+    lib.kvs_host_alloc.restype = c.c_int
+    lib.kvs_host_alloc.argtypes = [
+        c.c_size_t, c.c_int, c.c_int, c.POINTER(c.c_void_p), c.POINTER(c.c_void_p),
+    ]
+    lib.kvs_host_free.restype = c.c_int
+    lib.kvs_host_free.argtypes = [c.c_void_p]
+
+
+def load(path: Optional[os.PathLike] = None) -> ctypes.CDLL:
+    """Load (once) and type the native library; raise if it is unusable."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise NativeLibraryError(
+            f"{p} not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+        )
+    try:
+        lib = ctypes.CDLL(str(p))
+    except OSError as exc:
+        raise NativeLibraryError(f"cannot load {p}: {exc}") from exc
+    missing = [s for s in EXPORTED_SYMBOLS if not hasattr(lib, s)]
+    if missing:
+        raise NativeLibraryError(f"{p} lacks symbols {missing}")
+    _declare(lib)
+    if lib.kvs_abi_version() != 1:
+        raise NativeLibraryError(f"{p}: ABI {lib.kvs_abi_version()} != 1")
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def error_string(code: int) -> str:
+    return load().kvs_error_string(int(code)).decode()
+
+
+def check(code: int, what: str = "kvswap") -> None:
+    """Map a libkvswap return code onto the reference's exception types."""
+    if code == KVS_OK:
+        return
+    msg = f"{what}: {error_string(code)} (code {code})"
+    if code in (KVS_ERR_INVALID, KVS_ERR_ALIGN):
+        raise ValueError(msg)
+    if code == KVS_ERR_RANGE:
+        raise IndexError(msg)
+    if code == KVS_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise KvSwapCudaError(msg)

@@ -1,0 +1,506 @@
+// libkvswap — sm_100a KV-swap data plane behind the C ABI in include/kvswap.h.
+//
+// What the reference models, this file performs: SwapManager.dispatch
+// (pkg/src/kvswitch/swap.py:181-232) charges 12 us/op of dispatch plus
+// bytes/32000 per TransferOp (costmodel.py:17-31).  Here one kernel launch per
+// SwapPlan moves every TransferOp's blocks across all KV planes, straight
+// between HBM and mapped pinned host memory over PCIe, so the per-op dispatch
+// cost the paper attacks disappears: ops become kernel
+// parameters, not API calls.
+//
+// Work decomposition (one plan == one launch):
+//   plan blocks are numbered k = 0..B-1 in TransferOp order (the logical
+//   order _pair_extents emits, cpu_store.py:95-120).  Unit (k, plane) is one
+//   plane_chunk_bytes chunk; chunks are cut into 4 KiB "pieces"
+//   (32 lanes x 16 B x 8 in flight).  A persistent grid of warps walks pieces
+//   grid-stride, so at any instant all warps sweep one contiguous window of
+//   the plan: host-side addresses advance sequentially (long PCIe bursts,
+//   DRAM-page friendly) and each warp keeps 8 independent 16-B requests in
+//   flight — non-posted PCIe reads (swap-in) need ~100 KiB outstanding to
+//   cover the ~2 us round trip.
+#include <cuda_runtime.h>
+#include <cuda.h>
+
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "kvswap.h"
+
+namespace {
+
+constexpr int kVecBytes = 16;
+constexpr int kUnroll = 8;
+constexpr int kWarpBytes = 32 * kVecBytes;          // 512 B per warp-wide access
+constexpr int kPieceBytes = kWarpBytes * kUnroll;   // 4 KiB per warp iteration
+constexpr int kMaxThreads = 1024;
+
+// Op tables travel in the kernel's parameter buffer (<= 32 KiB on sm_70+ with
+// CUDA >= 12.1): no staging ring, no H2D copy, lifetime ends at launch.
+template <int CAP>
+struct SwapParams {
+  const uint64_t* planes;      // device array [num_planes] of plane bases
+  char* host;                  // device-usable base of the host pool
+  int64_t chunk;               // plane_chunk_bytes
+  int64_t stride;              // plane_block_stride
+  int64_t host_block;          // num_planes * chunk
+  uint32_t num_planes;
+  uint32_t pieces_per_chunk;   // ceil(chunk / 4 KiB)
+  uint32_t total_pieces;       // blocks * planes * pieces_per_chunk
+  int32_t n_ops;
+  uint32_t* done_flag;         // optional completion word
+  unsigned long long* ticket;  // monotone CTA-retire counter of this direction
+  unsigned long long ticket_base;
+  uint32_t seq;
+  int32_t op_end[CAP];         // inclusive prefix sum of TransferOp.blocks
+  int32_t op_gpu[CAP];         // TransferOp.gpu_start
+  int32_t op_cpu[CAP];         // TransferOp.cpu_start
+};
+
+__device__ __forceinline__ int4 ld_stream(const void* p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_plain(void* p, const int4& v) {
+  asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// DIR == KVS_DIR_OUT: HBM plane chunk -> host block image.
+// DIR == KVS_DIR_IN : host block image -> HBM plane chunk.
+template <int DIR, int CAP>
+__global__ void __launch_bounds__(kMaxThreads)
+    kvs_swap_kernel(const __grid_constant__ SwapParams<CAP> p) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+
+  int op = 0;
+  int32_t op_begin = 0;
+  for (uint32_t i = warp; i < p.total_pieces; i += nwarps) {
+    const uint32_t chunk_idx = i / p.pieces_per_chunk;
+    const uint32_t piece = i - chunk_idx * p.pieces_per_chunk;
+    const uint32_t k = chunk_idx / p.num_planes;  // plan-order block
+    const uint32_t plane = chunk_idx - k * p.num_planes;
+    // Pieces only move forward for a warp, so the op cursor only advances.
+    while (static_cast<int32_t>(k) >= p.op_end[op]) {
+      op_begin = p.op_end[op];
+      ++op;
+    }
+    const int64_t rel = static_cast<int64_t>(k) - op_begin;
+    const int64_t off = static_cast<int64_t>(piece) * kPieceBytes;
+    char* gpu = reinterpret_cast<char*>(__ldg(p.planes + plane)) +
+                (p.op_gpu[op] + rel) * p.stride + off;
+    char* host = p.host + (p.op_cpu[op] + rel) * p.host_block +
+                 static_cast<int64_t>(plane) * p.chunk + off;
+    const char* src = (DIR == KVS_DIR_OUT) ? gpu : host;
+    char* dst = (DIR == KVS_DIR_OUT) ? host : gpu;
+    const int64_t remain = p.chunk - off;
+    const uint32_t lo = lane * kVecBytes;
+
+    int4 v[kUnroll];
+    if (remain >= kPieceBytes) {
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) v[j] = ld_stream(src + j * kWarpBytes + lo);
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j) st_plain(dst + j * kWarpBytes + lo, v[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j)
+        if (j * kWarpBytes + lo < remain) v[j] = ld_stream(src + j * kWarpBytes + lo);
+#pragma unroll
+      for (int j = 0; j < kUnroll; ++j)
+        if (j * kWarpBytes + lo < remain) st_plain(dst + j * kWarpBytes + lo, v[j]);
+    }
+  }
+
+  if (p.done_flag != nullptr) {
+    // Last CTA to retire publishes `seq` with system-scope release, after
+    // every CTA fenced its stores (host-visible for swap-out).
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const unsigned long long t = atomicAdd(p.ticket, 1ull);
+      if (t == p.ticket_base + gridDim.x - 1) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.seq)
+                     : "memory");
+      }
+    }
+  }
+}
+
+}  // namespace
+
+struct KvsHandle {
+  int device = 0;
+  KvsGeometry geo{};
+  int64_t num_gpu_blocks = 0;
+  int64_t num_cpu_blocks = 0;
+  char* host = nullptr;
+  uint64_t* d_planes = nullptr;                 // device copy of plane bases
+  std::vector<uint64_t> h_planes;               // host copy (baselines)
+  unsigned long long* d_tickets = nullptr;      // [2] per-direction counters
+  unsigned long long ticket_next[2] = {0, 0};
+  int ctas[2] = {0, 0};
+  int threads[2] = {0, 0};
+  int64_t launches = 0;
+};
+
+namespace {
+
+int cuda_rc(cudaError_t e) { return e == cudaSuccess ? KVS_OK : static_cast<int>(e); }
+
+int default_ctas(int dir) { return dir == KVS_DIR_OUT ? 32 : 32; }
+constexpr int kDefaultThreads = 512;
+
+// Validate ops against both pools; fill op tables.  Returns KVS_OK or error.
+int check_ops(const KvsHandle* h, const int32_t* ops, int32_t n_ops, int64_t* total_blocks) {
+  int64_t total = 0;
+  for (int32_t i = 0; i < n_ops; ++i) {
+    const int64_t b = ops[3 * i], g = ops[3 * i + 1], c = ops[3 * i + 2];
+    if (b < 1) return KVS_ERR_INVALID;
+    if (g < 0 || g + b > h->num_gpu_blocks) return KVS_ERR_RANGE;
+    if (c < 0 || c + b > h->num_cpu_blocks) return KVS_ERR_RANGE;
+    total += b;
+  }
+  if (total > INT32_MAX) return KVS_ERR_RANGE;
+  *total_blocks = total;
+  return KVS_OK;
+}
+
+template <int CAP>
+int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t blocks,
+               cudaStream_t stream, uint32_t* done_flag, uint32_t seq) {
+  SwapParams<CAP> p;
+  p.planes = h->d_planes;
+  p.host = h->host;
+  p.chunk = h->geo.plane_chunk_bytes;
+  p.stride = h->geo.plane_block_stride;
+  p.host_block = h->geo.plane_chunk_bytes * h->geo.num_planes;
+  p.num_planes = static_cast<uint32_t>(h->geo.num_planes);
+  p.pieces_per_chunk =
+      static_cast<uint32_t>((h->geo.plane_chunk_bytes + kPieceBytes - 1) / kPieceBytes);
+  const uint64_t pieces = static_cast<uint64_t>(blocks) * p.num_planes * p.pieces_per_chunk;
+  if (pieces > 0xFFFFFFFFull) return KVS_ERR_RANGE;
+  p.total_pieces = static_cast<uint32_t>(pieces);
+  p.n_ops = n_ops;
+  int32_t run = 0;
+  for (int32_t i = 0; i < n_ops; ++i) {
+    run += ops[3 * i];
+    p.op_end[i] = run;
+    p.op_gpu[i] = ops[3 * i + 1];
+    p.op_cpu[i] = ops[3 * i + 2];
+  }
+  int threads = h->threads[dir] > 0 ? h->threads[dir] : kDefaultThreads;
+  int ctas = h->ctas[dir] > 0 ? h->ctas[dir] : default_ctas(dir);
+  // Never launch warps that can have no piece.
+  const uint64_t warps_needed = pieces;
+  const uint64_t warps_per_cta = static_cast<uint64_t>(threads) / 32;
+  const uint64_t max_ctas = (warps_needed + warps_per_cta - 1) / warps_per_cta;
+  if (static_cast<uint64_t>(ctas) > max_ctas) ctas = static_cast<int>(max_ctas);
+  if (ctas < 1) ctas = 1;
+  p.done_flag = done_flag;
+  p.ticket = h->d_tickets + dir;
+  p.ticket_base = h->ticket_next[dir];
+  p.seq = seq;
+  if (done_flag != nullptr) h->ticket_next[dir] += static_cast<unsigned long long>(ctas);
+  if (dir == KVS_DIR_OUT)
+    kvs_swap_kernel<KVS_DIR_OUT, CAP><<<ctas, threads, 0, stream>>>(p);
+  else
+    kvs_swap_kernel<KVS_DIR_IN, CAP><<<ctas, threads, 0, stream>>>(p);
+  h->launches += 1;
+  return cuda_rc(cudaGetLastError());
+}
+
+// One launch for <= 2048 ops, smallest parameter block that fits.
+int launch_one(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t blocks,
+               cudaStream_t stream, uint32_t* done_flag, uint32_t seq) {
+  if (n_ops <= 32) return launch_cap<32>(h, dir, ops, n_ops, blocks, stream, done_flag, seq);
+  if (n_ops <= 256) return launch_cap<256>(h, dir, ops, n_ops, blocks, stream, done_flag, seq);
+  return launch_cap<2048>(h, dir, ops, n_ops, blocks, stream, done_flag, seq);
+}
+constexpr int32_t kOpsPerLaunch = 2048;
+
+using StreamWaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using StreamWriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+template <typename Fn>
+Fn driver_fn(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<Fn>(fn);
+}
+
+struct HostAlloc {
+  size_t bytes;
+  int flags;
+};
+std::mutex g_host_mu;
+std::unordered_map<void*, HostAlloc> g_host_allocs;
+
+}  // namespace
+
+extern "C" {
+
+int kvs_abi_version(void) { return KVS_ABI_VERSION; }
+
+const char* kvs_error_string(int code) {
+  switch (code) {
+    case KVS_OK: return "ok";
+    case KVS_ERR_INVALID: return "kvswap: invalid argument";
+    case KVS_ERR_RANGE: return "kvswap: transfer op outside the GPU or host pool";
+    case KVS_ERR_ALIGN: return "kvswap: pointer or size not 16-byte aligned";
+    case KVS_ERR_NOMEM: return "kvswap: host allocation or pinning failed";
+    case KVS_ERR_UNSUPPORTED: return "kvswap: driver lacks a required feature";
+    default: break;
+  }
+  if (code > 0) return cudaGetErrorString(static_cast<cudaError_t>(code));
+  return "kvswap: unknown error";
+}
+
+int kvs_create(int device, const KvsGeometry* geo, const uint64_t* plane_ptrs, void* host_base,
+               int64_t num_gpu_blocks, int64_t num_cpu_blocks, KvsHandle** out) {
+  if (out == nullptr || geo == nullptr || plane_ptrs == nullptr || host_base == nullptr)
+    return KVS_ERR_INVALID;
+  *out = nullptr;
+  if (geo->num_planes < 1 || geo->reserved != 0 || geo->plane_chunk_bytes < kVecBytes ||
+      geo->plane_block_stride < geo->plane_chunk_bytes || num_gpu_blocks < 1 ||
+      num_cpu_blocks < 1 || device < 0)
+    return KVS_ERR_INVALID;
+  if (geo->plane_chunk_bytes % kVecBytes || geo->plane_block_stride % kVecBytes ||
+      reinterpret_cast<uintptr_t>(host_base) % kVecBytes)
+    return KVS_ERR_ALIGN;
+  for (int p = 0; p < geo->num_planes; ++p)
+    if (plane_ptrs[p] == 0 || plane_ptrs[p] % kVecBytes) return KVS_ERR_ALIGN;
+  int rc = cuda_rc(cudaSetDevice(device));
+  if (rc) return rc;
+  auto* h = new KvsHandle();
+  h->device = device;
+  h->geo = *geo;
+  h->num_gpu_blocks = num_gpu_blocks;
+  h->num_cpu_blocks = num_cpu_blocks;
+  h->host = static_cast<char*>(host_base);
+  h->h_planes.assign(plane_ptrs, plane_ptrs + geo->num_planes);
+  rc = cuda_rc(cudaMalloc(&h->d_planes, sizeof(uint64_t) * geo->num_planes));
+  if (!rc)
+    rc = cuda_rc(cudaMemcpy(h->d_planes, plane_ptrs, sizeof(uint64_t) * geo->num_planes,
+                            cudaMemcpyHostToDevice));
+  if (!rc) rc = cuda_rc(cudaMalloc(&h->d_tickets, 2 * sizeof(unsigned long long)));
+  if (!rc) rc = cuda_rc(cudaMemset(h->d_tickets, 0, 2 * sizeof(unsigned long long)));
+  if (rc) {
+    kvs_destroy(h);
+    return rc;
+  }
+  *out = h;
+  return KVS_OK;
+}
+
+int kvs_destroy(KvsHandle* h) {
+  if (h == nullptr) return KVS_OK;
+  cudaSetDevice(h->device);
+  if (h->d_planes) cudaFree(h->d_planes);
+  if (h->d_tickets) cudaFree(h->d_tickets);
+  delete h;
+  return KVS_OK;
+}
+
+int kvs_set_launch(KvsHandle* h, int dir, int ctas, int threads) {
+  if (h == nullptr || (dir != KVS_DIR_OUT && dir != KVS_DIR_IN)) return KVS_ERR_INVALID;
+  if (ctas < 0 || threads < 0 || threads % 32 || threads > kMaxThreads) return KVS_ERR_INVALID;
+  h->ctas[dir] = ctas;
+  h->threads[dir] = threads;
+  return KVS_OK;
+}
+
+int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
+             uint32_t* done_flag, uint32_t seq) {
+  if (h == nullptr || (dir != KVS_DIR_OUT && dir != KVS_DIR_IN) || n_ops < 0 ||
+      (n_ops > 0 && ops == nullptr))
+    return KVS_ERR_INVALID;
+  int64_t blocks = 0;
+  int rc = check_ops(h, ops, n_ops, &blocks);
+  if (rc) return rc;
+  rc = cuda_rc(cudaSetDevice(h->device));
+  if (rc) return rc;
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  if (n_ops == 0) {
+    if (done_flag == nullptr) return KVS_OK;
+    static auto write_fn = driver_fn<StreamWriteValue32Fn>("cuStreamWriteValue32");
+    if (write_fn == nullptr) return KVS_ERR_UNSUPPORTED;
+    return write_fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(done_flag), seq,
+                    0) == CUDA_SUCCESS
+               ? KVS_OK
+               : KVS_ERR_UNSUPPORTED;
+  }
+  for (int32_t first = 0; first < n_ops; first += kOpsPerLaunch) {
+    const int32_t n = (n_ops - first) < kOpsPerLaunch ? (n_ops - first) : kOpsPerLaunch;
+    int64_t part = 0;
+    for (int32_t i = 0; i < n; ++i) part += ops[3 * (first + i)];
+    const bool last = first + n == n_ops;
+    rc = launch_one(h, dir, ops + 3 * first, n, part, s, last ? done_flag : nullptr, seq);
+    if (rc) return rc;
+  }
+  return KVS_OK;
+}
+
+int kvs_wait_flag(uint64_t stream, const uint32_t* flag, uint32_t value) {
+  if (flag == nullptr) return KVS_ERR_INVALID;
+  static auto wait_fn = driver_fn<StreamWaitValue32Fn>("cuStreamWaitValue32");
+  if (wait_fn == nullptr) return KVS_ERR_UNSUPPORTED;
+  const CUresult r = wait_fn(reinterpret_cast<CUstream>(stream),
+                             reinterpret_cast<CUdeviceptr>(flag), value, CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? KVS_OK : KVS_ERR_UNSUPPORTED;
+}
+
+int64_t kvs_launch_count(const KvsHandle* h) { return h ? h->launches : -1; }
+
+int kvs_memcpy_baseline(KvsHandle* h, int dir, int mode, const int32_t* ops, int32_t n_ops,
+                        uint64_t stream) {
+  if (h == nullptr || (dir != KVS_DIR_OUT && dir != KVS_DIR_IN) || n_ops < 0 ||
+      (n_ops > 0 && ops == nullptr))
+    return KVS_ERR_INVALID;
+  int64_t blocks = 0;
+  int rc = check_ops(h, ops, n_ops, &blocks);
+  if (rc) return rc;
+  rc = cuda_rc(cudaSetDevice(h->device));
+  if (rc) return rc;
+  auto s = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t chunk = h->geo.plane_chunk_bytes, stride = h->geo.plane_block_stride;
+  const int64_t hblk = chunk * h->geo.num_planes;
+  const int P = h->geo.num_planes;
+  auto gpu_addr = [&](int p, int64_t b) {
+    return reinterpret_cast<char*>(h->h_planes[p]) + b * stride;
+  };
+  auto host_addr = [&](int p, int64_t c) { return h->host + c * hblk + p * chunk; };
+  if (mode == KVS_BASE_PER_BLOCK) {
+    // vLLM swap_blocks: per layer (plane), one cudaMemcpyAsync per block.
+    for (int p = 0; p < P; ++p)
+      for (int32_t i = 0; i < n_ops; ++i)
+        for (int32_t b = 0; b < ops[3 * i]; ++b) {
+          char* g = gpu_addr(p, ops[3 * i + 1] + b);
+          char* c = host_addr(p, ops[3 * i + 2] + b);
+          rc = cuda_rc(dir == KVS_DIR_OUT
+                           ? cudaMemcpyAsync(c, g, chunk, cudaMemcpyDeviceToHost, s)
+                           : cudaMemcpyAsync(g, c, chunk, cudaMemcpyHostToDevice, s));
+          if (rc) return rc;
+        }
+    return KVS_OK;
+  }
+  if (mode == KVS_BASE_PER_RUN) {
+    for (int p = 0; p < P; ++p)
+      for (int32_t i = 0; i < n_ops; ++i) {
+        char* g = gpu_addr(p, ops[3 * i + 1]);
+        char* c = host_addr(p, ops[3 * i + 2]);
+        const size_t rows = static_cast<size_t>(ops[3 * i]);
+        rc = cuda_rc(dir == KVS_DIR_OUT
+                         ? cudaMemcpy2DAsync(c, hblk, g, stride, chunk, rows,
+                                             cudaMemcpyDeviceToHost, s)
+                         : cudaMemcpy2DAsync(g, stride, c, hblk, chunk, rows,
+                                             cudaMemcpyHostToDevice, s));
+        if (rc) return rc;
+      }
+    return KVS_OK;
+  }
+  if (mode == KVS_BASE_BATCH) {
+    if (blocks == 0) return KVS_OK;
+    const size_t n = static_cast<size_t>(blocks) * P;
+    std::vector<void*> dsts(n), srcs(n);
+    std::vector<size_t> sizes(n, static_cast<size_t>(chunk));
+    size_t k = 0;
+    for (int32_t i = 0; i < n_ops; ++i)
+      for (int32_t b = 0; b < ops[3 * i]; ++b)
+        for (int p = 0; p < P; ++p, ++k) {
+          char* g = gpu_addr(p, ops[3 * i + 1] + b);
+          char* c = host_addr(p, ops[3 * i + 2] + b);
+          dsts[k] = dir == KVS_DIR_OUT ? static_cast<void*>(c) : static_cast<void*>(g);
+          srcs[k] = dir == KVS_DIR_OUT ? static_cast<void*>(g) : static_cast<void*>(c);
+        }
+    cudaMemcpyAttributes attr;
+    std::memset(&attr, 0, sizeof(attr));
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail_idx = 0;
+    return cuda_rc(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr,
+                                        &attr_idx, 1, &fail_idx, s));
+  }
+  return KVS_ERR_INVALID;
+}
+
+int kvs_host_alloc(size_t bytes, int numa_node, int flags, void** host, void** dev) {
+  if (host == nullptr || dev == nullptr || bytes == 0) return KVS_ERR_INVALID;
+  *host = nullptr;
+  *dev = nullptr;
+  void* p = nullptr;
+  if (flags == KVS_HOST_DEFAULT) {
+    int rc = cuda_rc(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+    if (rc) return rc;
+  } else if (flags == KVS_HOST_REGISTER) {
+    p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return KVS_ERR_NOMEM;
+    if (numa_node >= 0 && numa_node < 64) {
+      // MPOL_BIND = 2; pages are placed on first touch by cudaHostRegister.
+      unsigned long mask = 1ul << numa_node;
+      if (syscall(SYS_mbind, p, bytes, 2, &mask, 64, 0) != 0) {
+        munmap(p, bytes);
+        return KVS_ERR_NOMEM;
+      }
+    }
+    int rc = cuda_rc(
+        cudaHostRegister(p, bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+    if (rc) {
+      munmap(p, bytes);
+      return rc;
+    }
+  } else {
+    return KVS_ERR_INVALID;
+  }
+  void* d = nullptr;
+  int rc = cuda_rc(cudaHostGetDevicePointer(&d, p, 0));
+  if (rc) {
+    if (flags == KVS_HOST_DEFAULT) {
+      cudaFreeHost(p);
+    } else {
+      cudaHostUnregister(p);
+      munmap(p, bytes);
+    }
+    return rc;
+  }
+  {
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    g_host_allocs[p] = HostAlloc{bytes, flags};
+  }
+  *host = p;
+  *dev = d;
+  return KVS_OK;
+}
+
+int kvs_host_free(void* host) {
+  HostAlloc a;
+  {
+    std::lock_guard<std::mutex> lock(g_host_mu);
+    auto it = g_host_allocs.find(host);
+    if (it == g_host_allocs.end()) return KVS_ERR_INVALID;
+    a = it->second;
+    g_host_allocs.erase(it);
+  }
+  if (a.flags == KVS_HOST_DEFAULT) return cuda_rc(cudaFreeHost(host));
+  int rc = cuda_rc(cudaHostUnregister(host));
+  munmap(host, a.bytes);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,198 @@
+"""Real bytes under SwapManager.dispatch: device KV planes, the pinned host
+pool, and the libkvswap handle that moves SwapPlans between them.
+
+Reference seam: kvswitch models a swap as timestamps only
+(swap.py:181-232); the CPU copy is bookkeeping over host block groups
+(cpu_store.py:123-141).  This module owns the memory those blocks name:
+
+* `PagedKVCache` — the rank's GPU KV cache, one plane per layer (or two with
+  split K/V), allocated once in HBM by torch (it outlives every swap).
+* `HostKVPool` — the CpuStore's swap space: block-major, pinned, device-mapped
+  host memory from kvs_host_alloc (cudaHostAlloc Mapped|Portable or
+  mmap+mbind+cudaHostRegister).
+* `SwapDataPlane` — one kvs handle per rank; `swap()` queues one plan as one
+  kernel launch on a caller-chosen stream, `baseline()` queues the
+  copy-engine comparators.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Iterable, Optional, Sequence, Union
+
+import numpy as np
+import torch
+
+from . import _lib
+from .geometry import KVGeometry
+
+OpsLike = Union[np.ndarray, Sequence]
+
+
+def ops_array(ops: OpsLike) -> np.ndarray:
+    """TransferOp list / (blocks, gpu_start, cpu_start) tuples -> int32 [n, 3]."""
+    if isinstance(ops, np.ndarray):
+        arr = np.ascontiguousarray(ops, dtype=np.int32).reshape(-1, 3)
+        return arr
+    flat = []
+    for op in ops:
+        if hasattr(op, "blocks"):
+            flat.extend((op.blocks, op.gpu_start, op.cpu_start))
+        else:
+            b, g, c = op
+            flat.extend((b, g, c))
+    return np.asarray(flat, dtype=np.int32).reshape(-1, 3)
+
+
+def _stream_handle(stream: Optional[torch.cuda.Stream]) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+class HostKVPool:
+    """Pinned, device-mapped host swap space: [num_blocks, block_bytes] bytes."""
+
+    def __init__(self, num_blocks: int, block_bytes: int, numa_node: int = -1,
+                 register: bool = False) -> None:
+        if num_blocks < 1 or block_bytes < 16 or block_bytes % 16:
+            raise ValueError("host pool needs >= 1 block of a 16-byte multiple")
+        lib = _lib.load()
+        self.num_blocks = num_blocks
+        self.block_bytes = block_bytes
+        self.nbytes = num_blocks * block_bytes
+        host = ctypes.c_void_p()
+        dev = ctypes.c_void_p()
+        flags = _lib.KVS_HOST_REGISTER if register else _lib.KVS_HOST_DEFAULT
+        _lib.check(lib.kvs_host_alloc(self.nbytes, numa_node, flags,
+                                      ctypes.byref(host), ctypes.byref(dev)),
+                   "kvs_host_alloc")
+        self.host_ptr = int(host.value)
+        self.dev_ptr = int(dev.value)
+        buf = (ctypes.c_uint8 * self.nbytes).from_address(self.host_ptr)
+        self._buf = buf
+        self.array = np.frombuffer(buf, dtype=np.uint8).reshape(num_blocks, block_bytes)
+        self.tensor = torch.from_numpy(self.array)
+
+    def close(self) -> None:
+        if getattr(self, "host_ptr", 0):
+            self.tensor = None
+            self.array = None
+            self._buf = None
+            _lib.check(_lib.load().kvs_host_free(ctypes.c_void_p(self.host_ptr)), "kvs_host_free")
+            self.host_ptr = 0
+
+    def __del__(self) -> None:  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class PagedKVCache:
+    """The rank's KV cache in HBM: planes [P, num_blocks, chunk] of raw bytes.
+
+    `layer(l)` views plane l as the model's [num_blocks, 2, T, H, d] tensor.
+    """
+
+    def __init__(self, geometry: KVGeometry, num_blocks: int,
+                 device: Union[int, str, torch.device] = "cuda",
+                 dtype: torch.dtype = torch.float16) -> None:
+        if num_blocks < 1:
+            raise ValueError("num_blocks must be >= 1")
+        self.geometry = geometry
+        self.num_blocks = num_blocks
+        self.device = torch.device(device)
+        self.dtype = dtype
+        self.planes = torch.empty(
+            (geometry.num_planes, num_blocks, geometry.plane_chunk_bytes),
+            dtype=torch.uint8, device=self.device,
+        )
+
+    @property
+    def plane_stride(self) -> int:
+        return self.geometry.plane_chunk_bytes
+
+    def plane_ptrs(self) -> list[int]:
+        base = self.planes.data_ptr()
+        step = self.num_blocks * self.geometry.plane_chunk_bytes
+        return [base + p * step for p in range(self.geometry.num_planes)]
+
+    def layer(self, l: int) -> torch.Tensor:
+        g = self.geometry
+        if g.split_kv:
+            raise ValueError("split_kv caches expose planes, not fused layers")
+        return self.planes[l].view(self.dtype).view(
+            self.num_blocks, 2, g.block_tokens, g.heads_per_rank, g.head_dim)
+
+
+class SwapDataPlane:
+    """One libkvswap handle: moves SwapPlans between a PagedKVCache and a HostKVPool."""
+
+    def __init__(self, cache: PagedKVCache, host: HostKVPool,
+                 ctas: Optional[dict] = None, threads: Optional[dict] = None) -> None:
+        g = cache.geometry
+        if host.block_bytes != g.block_bytes:
+            raise ValueError(
+                f"host pool block {host.block_bytes} B != geometry block {g.block_bytes} B"
+            )
+        self.lib = _lib.load()
+        self.cache = cache
+        self.host = host
+        self.geometry = g
+        geo = _lib.KvsGeometry(g.num_planes, 0, g.plane_chunk_bytes, cache.plane_stride)
+        ptrs = (ctypes.c_uint64 * g.num_planes)(*cache.plane_ptrs())
+        handle = ctypes.c_void_p()
+        dev_index = cache.device.index if cache.device.index is not None else torch.cuda.current_device()
+        _lib.check(self.lib.kvs_create(dev_index, ctypes.byref(geo), ptrs,
+                                       ctypes.c_void_p(host.dev_ptr), cache.num_blocks,
+                                       host.num_blocks, ctypes.byref(handle)), "kvs_create")
+        self.handle = handle
+        self.device_index = dev_index
+        for direction, d in _lib.DIRECTIONS.items():
+            c = (ctas or {}).get(direction, 0)
+            t = (threads or {}).get(direction, 0)
+            self.set_launch(direction, c, t)
+
+    def set_launch(self, direction: str, ctas: int = 0, threads: int = 0) -> None:
+        _lib.check(self.lib.kvs_set_launch(self.handle, _lib.DIRECTIONS[direction], ctas, threads),
+                   "kvs_set_launch")
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.kvs_launch_count(self.handle))
+
+    def swap(self, direction: str, ops: OpsLike, stream: Optional[torch.cuda.Stream] = None,
+             done_flag: Optional[int] = None, seq: int = 0) -> np.ndarray:
+        """Queue one plan (all its TransferOps, all planes) as one kernel launch."""
+        arr = ops_array(ops)
+        rc = self.lib.kvs_swap(self.handle, _lib.DIRECTIONS[direction],
+                               arr.ctypes.data_as(ctypes.c_void_p), arr.shape[0],
+                               _stream_handle(stream),
+                               ctypes.c_void_p(done_flag) if done_flag else None,
+                               seq & 0xFFFFFFFF)
+        _lib.check(rc, f"kvs_swap({direction})")
+        return arr
+
+    def baseline(self, direction: str, mode: int, ops: OpsLike,
+                 stream: Optional[torch.cuda.Stream] = None) -> None:
+        arr = ops_array(ops)
+        rc = self.lib.kvs_memcpy_baseline(self.handle, _lib.DIRECTIONS[direction], mode,
+                                          arr.ctypes.data_as(ctypes.c_void_p), arr.shape[0],
+                                          _stream_handle(stream))
+        _lib.check(rc, f"kvs_memcpy_baseline({direction}, mode={mode})")
+
+    def wait_flag(self, stream: Optional[torch.cuda.Stream], flag_ptr: int, value: int) -> None:
+        _lib.check(self.lib.kvs_wait_flag(_stream_handle(stream), ctypes.c_void_p(flag_ptr),
+                                          value & 0xFFFFFFFF), "kvs_wait_flag")
+
+    def close(self) -> None:
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self.lib.kvs_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self) -> None:  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass

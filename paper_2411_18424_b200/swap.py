@@ -1,0 +1,378 @@
+"""Multithreading Swap Manager on real streams — drop-in for kvswitch.swap.
+
+Two layers, one object:
+
+1. The reference's bookkeeping, bit-exact (pkg/src/kvswitch/swap.py):
+   one serial dispatcher (+dispatch_per_op per op) feeding one copy pipeline
+   per direction (finish = max(dispatch, prev) + exec_time), per-op OpRecord
+   busy extents for D2H sources, half-open conflict detection,
+   max-over-blockers resolution, dispatch-queue yield, adaptive sync/async
+   (decide_mode) and the r_info window.  In replay mode these simulated
+   timestamps drive every engine decision, exactly as in the reference.
+
+2. The B200 execution layer (`StreamExecutor`): each dispatched plan is ONE
+   libkvswap kernel launch on a low-priority per-direction stream (the
+   paper's dispatch thread pool, becomes unnecessary: dispatch
+   is O(1) per plan).  Real hazards are enforced with CUDA events, independent
+   of simulated time:
+     * swap-out waits for the compute stream (the KV it reads was produced there);
+     * a transfer waits for any still-running opposite-direction transfer
+       whose GPU or host extents it would overwrite or read stale
+       (WAR/RAW/WAW; same-direction transfers are already stream-ordered);
+     * compute waits for transfers that write blocks it is about to read or
+       that still read blocks it is about to write (engine.py:411-414 conflict
+       stall and the swap-in completion of engine.py:376-384, made real).
+"""
+
+from __future__ import annotations
+
+from collections import deque
+from dataclasses import dataclass, field
+from typing import Iterable, Optional
+
+from .core import RequestId, SimTime, elapsed
+from .costmodel import TransferParams
+from .cpu_store import SwapPlan
+
+R_INFO_WINDOW = 64
+
+
+@dataclass
+class SwapEvent:
+    iteration: int
+    request: RequestId
+    direction: str
+    ops: int
+    blocks: int
+    dispatch_done: SimTime
+    exec_done: SimTime
+    conflicts: int = 0
+
+
+@dataclass
+class OpRecord:
+    """GPU extent [gpu_start, gpu_start+gpu_len) busy until exec_done (swap.py:36-42)."""
+
+    gpu_start: int
+    gpu_len: int
+    exec_done: SimTime
+
+
+@dataclass
+class InFlightSwap:
+    request: RequestId
+    direction: str
+    plan: SwapPlan
+    dispatch_done: SimTime
+    exec_done: SimTime
+    op_records: list[OpRecord]
+    transfer: Optional["TransferRecord"] = None  # real execution, when attached
+
+    def completed(self, clock: SimTime) -> bool:
+        return clock >= self.exec_done
+
+
+@dataclass
+class QueueState:
+    """waiting / running / swapped / ongoing_swap_in partition (swap.py:58-104)."""
+
+    waiting: list[RequestId] = field(default_factory=list)
+    running: list[RequestId] = field(default_factory=list)
+    swapped: list[RequestId] = field(default_factory=list)
+    ongoing_swap_in: list[RequestId] = field(default_factory=list)
+    r_info: deque = field(default_factory=lambda: deque(maxlen=R_INFO_WINDOW))
+
+    def _queues(self) -> dict[str, list[RequestId]]:
+        return {"waiting": self.waiting, "running": self.running,
+                "swapped": self.swapped, "ongoing_swap_in": self.ongoing_swap_in}
+
+    def location(self, req: RequestId) -> Optional[str]:
+        for name, q in self._queues().items():
+            if req in q:
+                return name
+        return None
+
+    def remove(self, req: RequestId) -> None:
+        for q in self._queues().values():
+            if req in q:
+                q.remove(req)
+
+    def move(self, req: RequestId, dst: str) -> None:
+        self.remove(req)
+        self._queues()[dst].append(req)
+
+    def validate_partition(self, live: Iterable[RequestId]) -> None:
+        seen: set[RequestId] = set()
+        for q in self._queues().values():
+            for req in q:
+                if req in seen:
+                    raise AssertionError(f"request {req} appears in two queues")
+                seen.add(req)
+        live = set(live)
+        if seen != live:
+            raise AssertionError(f"queues cover {sorted(seen)} but live set is {sorted(live)}")
+
+
+@dataclass
+class StrategyDecision:
+    mode: str  # "async" | "sync"
+    reason: str  # small_short_requests | long_transfers | idle_io | forced_sync
+
+
+def decide_mode(pending_drain: SimTime, pending_max_footprint: int, iter_estimate: SimTime,
+                sync_threshold_ratio: float, short_request_blocks: int,
+                forced: Optional[str] = None) -> StrategyDecision:
+    """Adaptive swap-in strategy (swap.py:113-135): absorb a quick drain of
+    small swap-ins as one stall; let long transfers overlap inference."""
+    if forced == "sync":
+        return StrategyDecision("sync", "forced_sync")
+    if pending_max_footprint == 0:
+        return StrategyDecision("async", "idle_io")
+    quick = pending_drain < sync_threshold_ratio * iter_estimate
+    if quick and pending_max_footprint < short_request_blocks:
+        return StrategyDecision("sync", "small_short_requests")
+    return StrategyDecision("async", "long_transfers")
+
+
+# --------------------------------------------------------------------------
+# Real execution
+# --------------------------------------------------------------------------
+
+def _overlaps(a: list[tuple[int, int]], b: list[tuple[int, int]]) -> bool:
+    for s0, n0 in a:
+        e0 = s0 + n0
+        for s1, n1 in b:
+            if s0 < s1 + n1 and s1 < e0:
+                return True
+    return False
+
+
+@dataclass
+class TransferRecord:
+    direction: str
+    gpu: list[tuple[int, int]]
+    host: list[tuple[int, int]]
+    event: object  # torch.cuda.Event
+    nbytes: int
+    refresh_bytes: int
+    start_event: object = None
+    done: bool = False
+
+    def poll(self) -> bool:
+        if not self.done and self.event.query():
+            self.done = True
+        return self.done
+
+
+COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
+
+
+class StreamExecutor:
+    """Real streams + event hazards around one SwapDataPlane (one rank)."""
+
+    def __init__(self, dataplane, compute_stream=None, copy_impl: str = "kernel",
+                 timing: bool = False) -> None:
+        import torch
+
+        if copy_impl not in COPY_IMPLS:
+            raise ValueError(f"copy_impl must be one of {COPY_IMPLS}")
+        self.torch = torch
+        self.dp = dataplane
+        dev = dataplane.cache.device
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
+            else (0, -1)
+        self.streams = {
+            "out": torch.cuda.Stream(device=dev, priority=0),
+            "in": torch.cuda.Stream(device=dev, priority=0),
+        }
+        self.compute = compute_stream if compute_stream is not None else \
+            torch.cuda.Stream(device=dev, priority=-1)
+        self.copy_impl = copy_impl
+        self.timing = timing
+        self.pending: list[TransferRecord] = []
+        self.history: list[TransferRecord] = []
+        self.bytes = {"out": 0, "in": 0}
+        self.refresh_bytes = 0
+        self.launches = 0
+        self.block_bytes = dataplane.geometry.block_bytes
+
+    def _prune(self) -> None:
+        self.pending = [r for r in self.pending if not r.poll()]
+
+    def submit(self, direction: str, ops, split_single: bool = False,
+               refresh_blocks: int = 0) -> TransferRecord:
+        torch = self.torch
+        self._prune()
+        gpu = [(op.gpu_start, op.blocks) for op in ops]
+        host = [(op.cpu_start, op.blocks) for op in ops]
+        stream = self.streams[direction]
+        if direction == "out":
+            stream.wait_stream(self.compute)
+        for r in self.pending:
+            if r.direction == direction:
+                continue  # same stream: already ordered
+            if direction == "out":
+                hazard = _overlaps(host, r.host) or (r.direction == "in" and _overlaps(gpu, r.gpu))
+            else:
+                hazard = (r.direction == "out" and _overlaps(host, r.host)) or _overlaps(gpu, r.gpu)
+            if hazard:
+                stream.wait_event(r.event)
+        start = None
+        if self.timing:
+            start = torch.cuda.Event(enable_timing=True)
+            start.record(stream)
+        if ops:
+            if self.copy_impl == "kernel":
+                self.dp.swap(direction, ops, stream=stream)
+                self.launches += 1
+            else:
+                mode = COPY_IMPLS.index(self.copy_impl) - 1
+                self.dp.baseline(direction, mode, ops, stream=stream)
+        ev = torch.cuda.Event(enable_timing=self.timing)
+        ev.record(stream)
+        blocks = sum(op.blocks for op in ops)
+        rec = TransferRecord(direction, gpu, host, ev, blocks * self.block_bytes,
+                             refresh_blocks * self.block_bytes, start)
+        self.bytes[direction] += rec.nbytes
+        self.refresh_bytes += rec.refresh_bytes
+        self.pending.append(rec)
+        if self.timing:
+            self.history.append(rec)
+        return rec
+
+    def compute_barrier(self, extents: list[tuple[int, int]]) -> int:
+        """Make the compute stream wait for transfers touching `extents`.
+
+        Returns the number of transfers waited on (real conflicts)."""
+        self._prune()
+        n = 0
+        for r in self.pending:
+            if _overlaps(extents, r.gpu):
+                self.compute.wait_event(r.event)
+                n += 1
+        return n
+
+    def wait_transfer(self, rec: TransferRecord) -> None:
+        self.compute.wait_event(rec.event)
+
+    def synchronize(self) -> None:
+        for s in self.streams.values():
+            s.synchronize()
+        self.compute.synchronize()
+        self._prune()
+
+
+class SwapManager:
+    """Dispatcher / copy-engine timelines and in-flight swaps (swap.py:138-285),
+    optionally executing every plan's bytes through a StreamExecutor."""
+
+    def __init__(self, params: TransferParams, split_ops_to_single_blocks: bool = False,
+                 bytes_per_block: int = 131072,
+                 executor: Optional[StreamExecutor] = None) -> None:
+        self.params = params
+        self.split_single = split_ops_to_single_blocks
+        self.bytes_per_block = bytes_per_block
+        self.executor = executor
+        self.dispatcher_free_at: SimTime = 0
+        self.ops_since_yield = 0
+        self.engine_free_at: dict[str, SimTime] = {"in": 0, "out": 0}
+        self.in_flight: list[InFlightSwap] = []
+        self.busy_extents: list[OpRecord] = []
+        self.events_log: list[SwapEvent] = []
+        self.total_ops = {"in": 0, "out": 0}
+        self.total_blocks = {"in": 0, "out": 0}
+
+    # step 1 --------------------------------------------------------------
+
+    def pop_completed(self, clock: SimTime) -> list[InFlightSwap]:
+        """Swaps whose (simulated) execution has finished, in (exec_done, request) order."""
+        finished, running = [], []
+        for s in self.in_flight:
+            (finished if s.exec_done <= clock else running).append(s)
+        self.in_flight = running
+        self.busy_extents = [r for r in self.busy_extents if r.exec_done > clock]
+        finished.sort(key=lambda s: (s.exec_done, s.request))
+        return finished
+
+    def pending_swap_ins(self) -> list[InFlightSwap]:
+        return [s for s in self.in_flight if s.direction == "in"]
+
+    # steps 2-3 -------------------------------------------------------------
+
+    def _op_sizes(self, plan: SwapPlan) -> list[tuple[int, int, int]]:
+        """(gpu_start, blocks, bytes) per issued op; one per block in split mode."""
+        bpb = self.bytes_per_block
+        if not self.split_single:
+            return [(op.gpu_start, op.blocks, op.blocks * bpb) for op in plan.ops]
+        return [(op.gpu_start + i, 1, bpb) for op in plan.ops for i in range(op.blocks)]
+
+    def dispatch(self, clock: SimTime, iteration: int, plan: SwapPlan,
+                 not_before: SimTime = 0) -> InFlightSwap:
+        """Queue a plan; `not_before` delays execution, never dispatch."""
+        p = self.params
+        issued = self._op_sizes(plan)
+        t_disp = max(clock, self.dispatcher_free_at)
+        t_exec = max(self.engine_free_at[plan.direction], not_before)
+        records: list[OpRecord] = []
+        for gpu_start, blocks, nbytes in issued:
+            t_disp += p.dispatch_per_op
+            t_exec = max(t_exec, t_disp) + p.exec_time(nbytes)
+            records.append(OpRecord(gpu_start, blocks, t_exec))
+        self.ops_since_yield = (self.ops_since_yield + len(issued)) % p.sync_batch
+        exec_done = t_exec if issued else max(clock, not_before)
+        self.dispatcher_free_at = t_disp
+        self.engine_free_at[plan.direction] = exec_done
+
+        flight = InFlightSwap(plan.request, plan.direction, plan, t_disp, exec_done, records)
+        if self.executor is not None:
+            flight.transfer = self.executor.submit(plan.direction, plan.all_ops(),
+                                                   split_single=self.split_single,
+                                                   refresh_blocks=plan.refresh_blocks)
+        self.in_flight.append(flight)
+        if plan.direction == "out":
+            self.busy_extents.extend(records)  # freed sources stay busy until exec_done
+        self.total_ops[plan.direction] += len(issued)
+        self.total_blocks[plan.direction] += plan.moved_blocks
+        self.events_log.append(SwapEvent(iteration, plan.request, plan.direction, len(issued),
+                                         plan.moved_blocks, t_disp, exec_done))
+        return flight
+
+    # step 3.1 --------------------------------------------------------------
+
+    def detect_conflicts(self, clock: SimTime, grants: list[tuple[int, int]]) -> list[OpRecord]:
+        """Busy D2H extents (exec_done > clock) intersecting any grant, half-open."""
+        hits = []
+        for start, length in grants:
+            end = start + length
+            for rec in self.busy_extents:
+                if rec.exec_done > clock and start < rec.gpu_start + rec.gpu_len \
+                        and rec.gpu_start < end:
+                    hits.append(rec)
+        return hits
+
+    @staticmethod
+    def resolve_conflicts(clock: SimTime, conflicts: list[OpRecord]) -> SimTime:
+        return max((elapsed(r.exec_done, clock) for r in conflicts), default=0)
+
+    def yield_stall(self, clock: SimTime) -> SimTime:
+        """Bounded wait for the dispatch queue's next yield point (swap.py:256-268)."""
+        if self.dispatcher_free_at <= clock:
+            return 0
+        p = self.params
+        backlog = -(-(self.dispatcher_free_at - clock) // p.dispatch_per_op)
+        to_yield = (p.sync_batch - self.ops_since_yield) % p.sync_batch
+        return min(backlog, to_yield) * p.dispatch_per_op
+
+    # r_info -----------------------------------------------------------------
+
+    def record_event(self, qs: QueueState, event: SwapEvent) -> None:
+        qs.r_info.append(event)
+
+    @staticmethod
+    def r_info_summary(qs: QueueState) -> dict[str, float]:
+        if not qs.r_info:
+            return {"events": 0, "ops": 0, "blocks": 0, "mean_exec_us": 0.0}
+        spans = [max(0, e.exec_done - e.dispatch_done) for e in qs.r_info]
+        return {"events": len(qs.r_info), "ops": sum(e.ops for e in qs.r_info),
+                "blocks": sum(e.blocks for e in qs.r_info),
+                "mean_exec_us": sum(spans) / len(spans)}

@@ -1,0 +1,213 @@
+"""GPU parity of the swap kernels (K1 swap-out gather, K2 swap-in scatter)
+against the oracle's TransferOp restatement (oracle/bytes_oracle.py), all
+through the C ABI (libkvswap.so via paper_2411_18424_b200.dataplane).
+
+Bar: bit-exact.  Small shapes are compared byte-for-byte with the numpy
+oracle; BASELINE-size shapes use the round-trip property
+(out -> poison HBM -> in to a different table == original).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import bytes_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _mk(torch, geometry, gpu_blocks, cpu_blocks, ctas=None):
+    from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
+
+    cache = PagedKVCache(geometry, gpu_blocks, device="cuda:0")
+    host = HostKVPool(cpu_blocks, geometry.block_bytes)
+    plane = SwapDataPlane(cache, host, ctas=ctas)
+    return cache, host, plane
+
+
+def _small_geometry(chunk_words=1028, planes=3):
+    from paper_2411_18424_b200.geometry import KVGeometry
+
+    # chunk = 2 (K,V) * 1 token * 1 head * d * 2 B = 4 * chunk_words bytes;
+    # 1028 words -> 4112 B is not a multiple of the 4 KiB piece, which
+    # exercises the ragged tail path.
+    return KVGeometry("tiny", num_layers=planes, num_kv_heads=1, head_dim=chunk_words,
+                      block_tokens=1)
+
+
+@pytest.mark.parametrize("chunk_words,planes", [(1028, 3), (1024, 2), (4, 1), (16400, 5)])
+def test_bitexact_vs_oracle_small(cuda_ok, chunk_words, planes):
+    torch = cuda_ok
+    geo = _small_geometry(chunk_words, planes)
+    G, C = 96, 80
+    cache, host, dp = _mk(torch, geo, G, C)
+    rng = np.random.default_rng(chunk_words)
+    pattern = orc.kv_pattern(7, geo.num_planes, G, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    host.array[:] = 0xAB
+    # a contiguous stretch (-> multi-block ops) inside otherwise random,
+    # duplicate-free tables
+    run_g, run_c = np.arange(50, 60), np.arange(30, 40)
+    gpu_tab = np.concatenate([orc.random_block_table(rng, 5, G, used=run_g), run_g])
+    gpu_tab = np.concatenate([gpu_tab, orc.random_block_table(rng, 25, G, used=gpu_tab)])
+    cpu_tab = np.concatenate([orc.random_block_table(rng, 5, C, used=run_c), run_c])
+    cpu_tab = np.concatenate([cpu_tab, orc.random_block_table(rng, 25, C, used=cpu_tab)])
+    assert len(set(gpu_tab)) == len(set(cpu_tab)) == 40
+    ops = orc.table_to_ops(gpu_tab, cpu_tab)
+    assert ops[:, 0].max() > 1
+
+    dp.swap("out", ops)
+    torch.cuda.synchronize()
+    want_host = np.full((C, geo.block_bytes), 0xAB, dtype=np.uint8)
+    orc.apply_plan("out", pattern.copy(), want_host, ops)
+    np.testing.assert_array_equal(host.array, want_host)
+
+    # swap-in to a different table over a poisoned pool
+    cache.planes.fill_(0xFF)
+    new_gpu = orc.random_block_table(rng, 40, G)
+    in_ops = orc.table_to_ops(new_gpu, cpu_tab)
+    dp.swap("in", in_ops)
+    torch.cuda.synchronize()
+    want_planes = np.full_like(pattern, 0xFF)
+    orc.apply_plan("in", want_planes, want_host, in_ops)
+    np.testing.assert_array_equal(cache.planes.cpu().numpy(), want_planes)
+    # and the logical content is the original one
+    got = cache.planes.cpu().numpy()
+    for k in range(40):
+        np.testing.assert_array_equal(got[:, new_gpu[k]], pattern[:, gpu_tab[k]])
+    host.close()
+
+
+def test_split_single_and_many_ops(cuda_ok):
+    """Baseline ablation ops (swap.py:170-179) and >2048-op plans (multi-launch)."""
+    torch = cuda_ok
+    geo = _small_geometry(64, 2)
+    G = C = 5000
+    cache, host, dp = _mk(torch, geo, G, C)
+    rng = np.random.default_rng(3)
+    pattern = orc.kv_pattern(11, geo.num_planes, G, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    gpu_tab = orc.random_block_table(rng, 4500, G)
+    cpu_tab = orc.random_block_table(rng, 4500, C)
+    ops = orc.table_to_ops(gpu_tab, cpu_tab)
+    assert len(ops) > 2048
+    single = orc.split_single(ops)
+    host.array[:] = 0
+    dp.swap("out", single)
+    torch.cuda.synchronize()
+    want = np.zeros((C, geo.block_bytes), dtype=np.uint8)
+    orc.apply_plan("out", pattern, want, ops)
+    np.testing.assert_array_equal(host.array, want)
+    host.close()
+
+
+def test_empty_and_bad_ops(cuda_ok):
+    torch = cuda_ok
+    geo = _small_geometry(64, 2)
+    cache, host, dp = _mk(torch, geo, 16, 16)
+    before = dp.launches
+    dp.swap("out", np.zeros((0, 3), dtype=np.int32))
+    assert dp.launches == before  # nothing to move, nothing launched
+    with pytest.raises(IndexError):
+        dp.swap("out", [(4, 14, 0)])  # GPU side past the pool
+    with pytest.raises(IndexError):
+        dp.swap("in", [(4, 0, 13)])  # host side past the pool
+    with pytest.raises(ValueError):
+        dp.swap("out", [(0, 0, 0)])  # zero-block op
+    with pytest.raises(KeyError):
+        dp.swap("sideways", [(1, 0, 0)])
+    host.close()
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_copy_engine_baselines_match(cuda_ok, mode):
+    """K3 per-block / per-run and K4 batch comparators move the same bytes."""
+    torch = cuda_ok
+    geo = _small_geometry(256, 4)
+    G, C = 128, 128
+    cache, host, dp = _mk(torch, geo, G, C)
+    rng = np.random.default_rng(mode)
+    pattern = orc.kv_pattern(5, geo.num_planes, G, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    ops = orc.random_runs(rng, 64, 8, G, C)
+    s = torch.cuda.Stream()
+    host.array[:] = 0
+    dp.baseline("out", mode, ops, stream=s)
+    s.synchronize()
+    want = np.zeros((C, geo.block_bytes), dtype=np.uint8)
+    orc.apply_plan("out", pattern, want, ops)
+    np.testing.assert_array_equal(host.array, want)
+    cache.planes.zero_()
+    dp.baseline("in", mode, ops, stream=s)
+    s.synchronize()
+    want_planes = np.zeros_like(pattern)
+    orc.apply_plan("in", want_planes, want, ops)
+    np.testing.assert_array_equal(cache.planes.cpu().numpy(), want_planes)
+    host.close()
+
+
+def test_done_flag_orders_streams(cuda_ok):
+    """kvs_swap's done flag + kvs_wait_flag: a consumer stream waits for the
+    swap-out before reusing its source blocks (engine.py:712-719 dependency)."""
+    torch = cuda_ok
+    geo = _small_geometry(1024, 4)
+    G = C = 512
+    cache, host, dp = _mk(torch, geo, G, C, ctas={"out": 2})
+    pattern = orc.kv_pattern(9, geo.num_planes, G, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda:0")
+    out_s, in_s = torch.cuda.Stream(), torch.cuda.Stream()
+    ops = [(G, 0, 0)]
+    for seq in (1, 2, 3):
+        dp.swap("out", ops, stream=out_s, done_flag=flag.data_ptr(), seq=seq)
+        dp.wait_flag(in_s, flag.data_ptr(), seq)
+        with torch.cuda.stream(in_s):
+            cache.planes.fill_(seq)  # overwrite the freed source blocks
+        torch.cuda.synchronize()
+        assert int(flag.item()) == seq
+        if seq == 1:
+            want = np.zeros((C, geo.block_bytes), dtype=np.uint8)
+            orc.apply_plan("out", pattern, want, ops)
+            np.testing.assert_array_equal(host.array, want)
+        else:
+            assert (host.array == seq - 1).all()
+    host.close()
+
+
+def test_config1_round_trip_llama3_8b(cuda_ok):
+    """BASELINE config 1 at full size: 64 requests, LLaMA-3-8B KV shape
+    (2 MiB blocks), footprints U{1..128}, fragmented random block tables,
+    swap all out, poison HBM, swap all back into fresh tables."""
+    torch = cuda_ok
+    from paper_2411_18424_b200.geometry import LLAMA3_8B
+
+    G = C = 8192
+    cache, host, dp = _mk(torch, LLAMA3_8B, G, C)
+    gen = torch.Generator(device="cuda:0").manual_seed(0)
+    cache.planes.view(torch.int32).random_(generator=gen)
+    rng = np.random.default_rng(0)
+    foot = rng.integers(1, 129, size=64)
+    total = int(foot.sum())
+    gpu_tab = orc.random_block_table(rng, total, G)
+    cpu_tab = orc.random_block_table(rng, total, C)
+    bounds = np.concatenate([[0], np.cumsum(foot)])
+    original = cache.planes[:, torch.from_numpy(gpu_tab).cuda()].clone()
+    s_out, s_in = torch.cuda.Stream(), torch.cuda.Stream()
+    for r in range(64):
+        lo, hi = bounds[r], bounds[r + 1]
+        dp.swap("out", orc.table_to_ops(gpu_tab[lo:hi], cpu_tab[lo:hi]), stream=s_out)
+    torch.cuda.synchronize()
+    # host image spot check against the GPU source (oracle pairing)
+    sample = rng.choice(total, size=64, replace=False)
+    for k in sample:
+        got = host.array[cpu_tab[k]].reshape(LLAMA3_8B.num_planes, -1)
+        want = original[:, k].cpu().numpy()
+        np.testing.assert_array_equal(got, want)
+    cache.planes.fill_(0xFF)
+    new_tab = orc.random_block_table(rng, total, G)
+    for r in range(64):
+        lo, hi = bounds[r], bounds[r + 1]
+        dp.swap("in", orc.table_to_ops(new_tab[lo:hi], cpu_tab[lo:hi]), stream=s_in)
+    torch.cuda.synchronize()
+    back = cache.planes[:, torch.from_numpy(new_tab).cuda()]
+    assert torch.equal(back, original)
+    host.close()
