@@ -203,6 +203,7 @@ def test_config1_round_trip_llama3_8b(cuda_ok):
         want = original[:, k].cpu().numpy()
         np.testing.assert_array_equal(got, want)
     cache.planes.fill_(0xFF)
+    torch.cuda.synchronize()  # the poison runs on torch's stream, the swaps on s_in
     new_tab = orc.random_block_table(rng, total, G)
     for r in range(64):
         lo, hi = bounds[r], bounds[r + 1]
