@@ -57,6 +57,10 @@ extern "C" {
 #define KVS_BASE_PER_RUN 1   /* block groups on the CE: one cudaMemcpy2DAsync per (plane, op) */
 #define KVS_BASE_BATCH 2     /* one cudaMemcpyBatchAsync per plan (CUDA >= 12.8)  */
 
+/* Kernel paths (kvs_set_path). */
+#define KVS_PATH_LSU 0  /* v1: warps move 16-B vectors with LDG/STG (default)       */
+#define KVS_PATH_BULK 1 /* v2: TMA bulk copies (cp.async.bulk) through an smem ring */
+
 /* kvs_host_alloc flags */
 #define KVS_HOST_DEFAULT 0
 #define KVS_HOST_REGISTER 1 /* mmap + (optional) mbind + cudaHostRegister instead of cudaHostAlloc */
@@ -93,6 +97,10 @@ int kvs_destroy(KvsHandle* h);
  * 0 = default).  Bounded footprint keeps decode SMs free (swap.py:256-268
  * yield analogue). */
 int kvs_set_launch(KvsHandle* h, int dir, int ctas, int threads);
+
+/* Select the kernel path for one direction.  piece_bytes / stages tune the
+ * bulk path's smem ring (0 = defaults: 16 KiB x 4); ignored by the LSU path. */
+int kvs_set_path(KvsHandle* h, int dir, int path, int piece_bytes, int stages);
 
 /* Queue one SwapPlan's bytes on `stream` — asynchronous, no host blocking,
  * no allocation.  Replaces the modeled copy-engine timeline of

@@ -30,6 +30,10 @@ KVS_BASE_PER_BLOCK = 0
 KVS_BASE_PER_RUN = 1
 KVS_BASE_BATCH = 2
 
+KVS_PATH_LSU = 0
+KVS_PATH_BULK = 1
+PATHS = {"lsu": KVS_PATH_LSU, "bulk": KVS_PATH_BULK}
+
 KVS_HOST_DEFAULT = 0
 KVS_HOST_REGISTER = 1
 
@@ -40,6 +44,7 @@ EXPORTED_SYMBOLS = (
     "kvs_create",
     "kvs_destroy",
     "kvs_set_launch",
+    "kvs_set_path",
     "kvs_swap",
     "kvs_wait_flag",
     "kvs_launch_count",
@@ -86,6 +91,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_destroy.argtypes = [c.c_void_p]
     lib.kvs_set_launch.restype = c.c_int
     lib.kvs_set_launch.argtypes = [c.c_void_p, c.c_int, c.c_int, c.c_int]
+    lib.kvs_set_path.restype = c.c_int
+    lib.kvs_set_path.argtypes = [c.c_void_p, c.c_int, c.c_int, c.c_int, c.c_int]
     lib.kvs_swap.restype = c.c_int
     lib.kvs_swap.argtypes = [
         c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64, c.c_void_p, c.c_uint32,

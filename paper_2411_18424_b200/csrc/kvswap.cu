@@ -58,6 +58,8 @@ struct SwapParams {
   unsigned long long* ticket;  // monotone CTA-retire counter of this direction
   unsigned long long ticket_base;
   uint32_t seq;
+  uint32_t piece_bytes;        // bulk path: bytes per TMA piece (16-B multiple)
+  uint32_t stages;             // bulk path: smem ring depth
   int32_t op_end[CAP];         // inclusive prefix sum of TransferOp.blocks
   int32_t op_gpu[CAP];         // TransferOp.gpu_start
   int32_t op_cpu[CAP];         // TransferOp.cpu_start
@@ -141,6 +143,152 @@ __global__ void __launch_bounds__(kMaxThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bulk path (v2): TMA bulk copies staged through shared memory.
+// One elected thread per CTA drives a ring of `stages` smem buffers:
+//   cp.async.bulk global->shared (mbarrier complete_tx)  then
+//   cp.async.bulk shared->global (bulk_group), with the ring slot recycled
+//   once the store has finished reading it (wait_group.read).
+// Either side may be host-mapped memory; the TMA engine, not the SM's LSU,
+// generates the traffic (SASS: UBLKCP).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+constexpr int kMaxStages = 16;
+
+// Resolve piece `i` of the plan into (src, dst, bytes) for direction DIR.
+template <int DIR, int CAP>
+__device__ __forceinline__ uint32_t bulk_piece(const SwapParams<CAP>& p, uint32_t i, int& op,
+                                               int32_t& op_begin, const char*& src, char*& dst) {
+  const uint32_t chunk_idx = i / p.pieces_per_chunk;
+  const uint32_t piece = i - chunk_idx * p.pieces_per_chunk;
+  const uint32_t k = chunk_idx / p.num_planes;
+  const uint32_t plane = chunk_idx - k * p.num_planes;
+  while (static_cast<int32_t>(k) >= p.op_end[op]) {
+    op_begin = p.op_end[op];
+    ++op;
+  }
+  const int64_t rel = static_cast<int64_t>(k) - op_begin;
+  const int64_t off = static_cast<int64_t>(piece) * p.piece_bytes;
+  char* gpu = reinterpret_cast<char*>(p.planes[plane]) + (p.op_gpu[op] + rel) * p.stride + off;
+  char* host = p.host + (p.op_cpu[op] + rel) * p.host_block +
+               static_cast<int64_t>(plane) * p.chunk + off;
+  src = (DIR == KVS_DIR_OUT) ? gpu : host;
+  dst = (DIR == KVS_DIR_OUT) ? host : gpu;
+  const int64_t remain = p.chunk - off;
+  return static_cast<uint32_t>(remain < p.piece_bytes ? remain : p.piece_bytes);
+}
+
+template <int DIR, int CAP>
+__global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant__ SwapParams<CAP> p) {
+  extern __shared__ __align__(128) char ring[];
+  __shared__ __align__(8) uint64_t bars[kMaxStages];
+  if (threadIdx.x == 0) {
+    const uint32_t S = p.stages;
+    for (uint32_t s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // Pieces of this CTA: blockIdx.x + j * gridDim.x, j = 0..n-1.
+    const uint32_t first = blockIdx.x;
+    const uint32_t n =
+        first < p.total_pieces ? (p.total_pieces - first + gridDim.x - 1) / gridDim.x : 0;
+    int lop = 0, sop = 0;          // op cursors: loads run ahead of stores
+    int32_t lbeg = 0, sbeg = 0;
+    uint32_t phase_bits = 0;
+    const uint32_t pre = n < S - 1 ? n : S - 1;
+    for (uint32_t j = 0; j < pre; ++j) {
+      const char* src;
+      char* dst;
+      const uint32_t b = bulk_piece<DIR>(p, first + j * gridDim.x, lop, lbeg, src, dst);
+      mbar_expect_tx(&bars[j % S], b);
+      bulk_load(ring + (j % S) * p.piece_bytes, src, b, &bars[j % S]);
+    }
+    for (uint32_t j = 0; j < n; ++j) {
+      const uint32_t slot = j % S;
+      const char* src;
+      char* dst;
+      const uint32_t b = bulk_piece<DIR>(p, first + j * gridDim.x, sop, sbeg, src, dst);
+      mbar_wait(&bars[slot], (phase_bits >> slot) & 1u);
+      phase_bits ^= 1u << slot;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_store(dst, ring + slot * p.piece_bytes, b);
+      const uint32_t jj = j + S - 1;
+      if (jj < n) {
+        // slot jj % S was last read by store j-1: allow only store j in flight.
+        bulk_wait_read<1>();
+        const char* s2;
+        char* d2;
+        const uint32_t b2 = bulk_piece<DIR>(p, first + jj * gridDim.x, lop, lbeg, s2, d2);
+        mbar_expect_tx(&bars[jj % S], b2);
+        bulk_load(ring + (jj % S) * p.piece_bytes, s2, b2, &bars[jj % S]);
+      }
+    }
+    bulk_wait_all();
+  }
+  if (p.done_flag != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      const unsigned long long t = atomicAdd(p.ticket, 1ull);
+      if (t == p.ticket_base + gridDim.x - 1) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.seq)
+                     : "memory");
+      }
+    }
+  }
+}
+
 }  // namespace
 
 struct KvsHandle {
@@ -155,6 +303,9 @@ struct KvsHandle {
   unsigned long long ticket_next[2] = {0, 0};
   int ctas[2] = {0, 0};
   int threads[2] = {0, 0};
+  int path[2] = {KVS_PATH_LSU, KVS_PATH_LSU};
+  int piece_bytes[2] = {0, 0};
+  int stages[2] = {0, 0};
   int64_t launches = 0;
 };
 
@@ -164,6 +315,9 @@ int cuda_rc(cudaError_t e) { return e == cudaSuccess ? KVS_OK : static_cast<int>
 
 int default_ctas(int dir) { return dir == KVS_DIR_OUT ? 32 : 32; }
 constexpr int kDefaultThreads = 512;
+constexpr int kDefaultBulkPiece = 16384;
+constexpr int kDefaultStages = 4;
+constexpr int kDefaultBulkCtas = 64;
 
 // Validate ops against both pools; fill op tables.  Returns KVS_OK or error.
 int check_ops(const KvsHandle* h, const int32_t* ops, int32_t n_ops, int64_t* total_blocks) {
@@ -190,8 +344,17 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   p.stride = h->geo.plane_block_stride;
   p.host_block = h->geo.plane_chunk_bytes * h->geo.num_planes;
   p.num_planes = static_cast<uint32_t>(h->geo.num_planes);
-  p.pieces_per_chunk =
-      static_cast<uint32_t>((h->geo.plane_chunk_bytes + kPieceBytes - 1) / kPieceBytes);
+  const bool bulk = h->path[dir] == KVS_PATH_BULK;
+  int64_t piece = kPieceBytes;
+  uint32_t stages = 0;
+  if (bulk) {
+    piece = h->piece_bytes[dir] > 0 ? h->piece_bytes[dir] : kDefaultBulkPiece;
+    if (piece > h->geo.plane_chunk_bytes) piece = h->geo.plane_chunk_bytes;
+    stages = h->stages[dir] > 0 ? static_cast<uint32_t>(h->stages[dir]) : kDefaultStages;
+  }
+  p.piece_bytes = static_cast<uint32_t>(piece);
+  p.stages = stages;
+  p.pieces_per_chunk = static_cast<uint32_t>((h->geo.plane_chunk_bytes + piece - 1) / piece);
   const uint64_t pieces = static_cast<uint64_t>(blocks) * p.num_planes * p.pieces_per_chunk;
   if (pieces > 0xFFFFFFFFull) return KVS_ERR_RANGE;
   p.total_pieces = static_cast<uint32_t>(pieces);
@@ -203,12 +366,11 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
     p.op_gpu[i] = ops[3 * i + 1];
     p.op_cpu[i] = ops[3 * i + 2];
   }
-  int threads = h->threads[dir] > 0 ? h->threads[dir] : kDefaultThreads;
-  int ctas = h->ctas[dir] > 0 ? h->ctas[dir] : default_ctas(dir);
-  // Never launch warps that can have no piece.
-  const uint64_t warps_needed = pieces;
-  const uint64_t warps_per_cta = static_cast<uint64_t>(threads) / 32;
-  const uint64_t max_ctas = (warps_needed + warps_per_cta - 1) / warps_per_cta;
+  int threads = bulk ? 32 : (h->threads[dir] > 0 ? h->threads[dir] : kDefaultThreads);
+  int ctas = h->ctas[dir] > 0 ? h->ctas[dir] : (bulk ? kDefaultBulkCtas : default_ctas(dir));
+  // Never launch warps (bulk: CTAs) that can have no piece.
+  const uint64_t units_per_cta = bulk ? 1 : static_cast<uint64_t>(threads) / 32;
+  const uint64_t max_ctas = (pieces + units_per_cta - 1) / units_per_cta;
   if (static_cast<uint64_t>(ctas) > max_ctas) ctas = static_cast<int>(max_ctas);
   if (ctas < 1) ctas = 1;
   p.done_flag = done_flag;
@@ -216,10 +378,19 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   p.ticket_base = h->ticket_next[dir];
   p.seq = seq;
   if (done_flag != nullptr) h->ticket_next[dir] += static_cast<unsigned long long>(ctas);
-  if (dir == KVS_DIR_OUT)
+  if (bulk) {
+    const size_t smem = static_cast<size_t>(stages) * static_cast<size_t>(piece);
+    auto kern = dir == KVS_DIR_OUT ? kvs_swap_bulk_kernel<KVS_DIR_OUT, CAP>
+                                   : kvs_swap_bulk_kernel<KVS_DIR_IN, CAP>;
+    int rc = cuda_rc(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+    if (rc) return rc;
+    kern<<<ctas, 32, smem, stream>>>(p);
+  } else if (dir == KVS_DIR_OUT) {
     kvs_swap_kernel<KVS_DIR_OUT, CAP><<<ctas, threads, 0, stream>>>(p);
-  else
+  } else {
     kvs_swap_kernel<KVS_DIR_IN, CAP><<<ctas, threads, 0, stream>>>(p);
+  }
   h->launches += 1;
   return cuda_rc(cudaGetLastError());
 }
@@ -324,6 +495,20 @@ int kvs_set_launch(KvsHandle* h, int dir, int ctas, int threads) {
   if (ctas < 0 || threads < 0 || threads % 32 || threads > kMaxThreads) return KVS_ERR_INVALID;
   h->ctas[dir] = ctas;
   h->threads[dir] = threads;
+  return KVS_OK;
+}
+
+int kvs_set_path(KvsHandle* h, int dir, int path, int piece_bytes, int stages) {
+  if (h == nullptr || (dir != KVS_DIR_OUT && dir != KVS_DIR_IN)) return KVS_ERR_INVALID;
+  if (path != KVS_PATH_LSU && path != KVS_PATH_BULK) return KVS_ERR_INVALID;
+  if (piece_bytes < 0 || piece_bytes % kVecBytes || piece_bytes > (1 << 17)) return KVS_ERR_INVALID;
+  if (stages < 0 || stages == 1 || stages > kMaxStages) return KVS_ERR_INVALID;
+  const int s = stages > 0 ? stages : kDefaultStages;
+  const int pb = piece_bytes > 0 ? piece_bytes : kDefaultBulkPiece;
+  if (path == KVS_PATH_BULK && static_cast<int64_t>(s) * pb > 227 * 1024) return KVS_ERR_INVALID;
+  h->path[dir] = path;
+  h->piece_bytes[dir] = piece_bytes;
+  h->stages[dir] = stages;
   return KVS_OK;
 }
 

@@ -158,6 +158,12 @@ class SwapDataPlane:
         _lib.check(self.lib.kvs_set_launch(self.handle, _lib.DIRECTIONS[direction], ctas, threads),
                    "kvs_set_launch")
 
+    def set_path(self, direction: str, path: str = "lsu", piece_bytes: int = 0,
+                 stages: int = 0) -> None:
+        """Kernel path per direction: "lsu" (16-B vector LDG/STG) or "bulk" (TMA)."""
+        _lib.check(self.lib.kvs_set_path(self.handle, _lib.DIRECTIONS[direction],
+                                         _lib.PATHS[path], piece_bytes, stages), "kvs_set_path")
+
     @property
     def launches(self) -> int:
         return int(self.lib.kvs_launch_count(self.handle))

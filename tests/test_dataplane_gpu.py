@@ -15,13 +15,18 @@ from oracle import bytes_oracle as orc
 pytestmark = pytest.mark.gpu
 
 
-def _mk(torch, geometry, gpu_blocks, cpu_blocks, ctas=None):
+def _mk(torch, geometry, gpu_blocks, cpu_blocks, ctas=None, path="lsu", piece=0, stages=0):
     from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
 
     cache = PagedKVCache(geometry, gpu_blocks, device="cuda:0")
     host = HostKVPool(cpu_blocks, geometry.block_bytes)
     plane = SwapDataPlane(cache, host, ctas=ctas)
+    for d in ("out", "in"):
+        plane.set_path(d, path, piece, stages)
     return cache, host, plane
+
+
+PATHS = [("lsu", 0, 0), ("bulk", 0, 0), ("bulk", 4096, 2), ("bulk", 32768, 6)]
 
 
 def _small_geometry(chunk_words=1028, planes=3):
@@ -34,12 +39,13 @@ def _small_geometry(chunk_words=1028, planes=3):
                       block_tokens=1)
 
 
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: f"{p[0]}-{p[1]}-{p[2]}")
 @pytest.mark.parametrize("chunk_words,planes", [(1028, 3), (1024, 2), (4, 1), (16400, 5)])
-def test_bitexact_vs_oracle_small(cuda_ok, chunk_words, planes):
+def test_bitexact_vs_oracle_small(cuda_ok, chunk_words, planes, path):
     torch = cuda_ok
     geo = _small_geometry(chunk_words, planes)
     G, C = 96, 80
-    cache, host, dp = _mk(torch, geo, G, C)
+    cache, host, dp = _mk(torch, geo, G, C, path=path[0], piece=path[1], stages=path[2])
     rng = np.random.default_rng(chunk_words)
     pattern = orc.kv_pattern(7, geo.num_planes, G, geo.plane_chunk_bytes)
     cache.planes.copy_(torch.from_numpy(pattern))
@@ -77,12 +83,13 @@ def test_bitexact_vs_oracle_small(cuda_ok, chunk_words, planes):
     host.close()
 
 
-def test_split_single_and_many_ops(cuda_ok):
+@pytest.mark.parametrize("path", ["lsu", "bulk"])
+def test_split_single_and_many_ops(cuda_ok, path):
     """Baseline ablation ops (swap.py:170-179) and >2048-op plans (multi-launch)."""
     torch = cuda_ok
     geo = _small_geometry(64, 2)
     G = C = 5000
-    cache, host, dp = _mk(torch, geo, G, C)
+    cache, host, dp = _mk(torch, geo, G, C, path=path)
     rng = np.random.default_rng(3)
     pattern = orc.kv_pattern(11, geo.num_planes, G, geo.plane_chunk_bytes)
     cache.planes.copy_(torch.from_numpy(pattern))
@@ -115,6 +122,10 @@ def test_empty_and_bad_ops(cuda_ok):
         dp.swap("out", [(0, 0, 0)])  # zero-block op
     with pytest.raises(KeyError):
         dp.swap("sideways", [(1, 0, 0)])
+    with pytest.raises(ValueError):
+        dp.set_path("out", "bulk", piece_bytes=100)  # not a 16-B multiple
+    with pytest.raises(ValueError):
+        dp.set_path("out", "bulk", piece_bytes=65536, stages=8)  # > 227 KiB smem
     host.close()
 
 
@@ -145,13 +156,14 @@ def test_copy_engine_baselines_match(cuda_ok, mode):
     host.close()
 
 
-def test_done_flag_orders_streams(cuda_ok):
+@pytest.mark.parametrize("path", ["lsu", "bulk"])
+def test_done_flag_orders_streams(cuda_ok, path):
     """kvs_swap's done flag + kvs_wait_flag: a consumer stream waits for the
     swap-out before reusing its source blocks (engine.py:712-719 dependency)."""
     torch = cuda_ok
     geo = _small_geometry(1024, 4)
     G = C = 512
-    cache, host, dp = _mk(torch, geo, G, C, ctas={"out": 2})
+    cache, host, dp = _mk(torch, geo, G, C, ctas={"out": 2}, path=path)
     pattern = orc.kv_pattern(9, geo.num_planes, G, geo.plane_chunk_bytes)
     cache.planes.copy_(torch.from_numpy(pattern))
     flag = torch.zeros(1, dtype=torch.int32, device="cuda:0")
@@ -173,7 +185,8 @@ def test_done_flag_orders_streams(cuda_ok):
     host.close()
 
 
-def test_config1_round_trip_llama3_8b(cuda_ok):
+@pytest.mark.parametrize("path", ["lsu", "bulk"])
+def test_config1_round_trip_llama3_8b(cuda_ok, path):
     """BASELINE config 1 at full size: 64 requests, LLaMA-3-8B KV shape
     (2 MiB blocks), footprints U{1..128}, fragmented random block tables,
     swap all out, poison HBM, swap all back into fresh tables."""
@@ -181,7 +194,7 @@ def test_config1_round_trip_llama3_8b(cuda_ok):
     from paper_2411_18424_b200.geometry import LLAMA3_8B
 
     G = C = 8192
-    cache, host, dp = _mk(torch, LLAMA3_8B, G, C)
+    cache, host, dp = _mk(torch, LLAMA3_8B, G, C, path=path)
     gen = torch.Generator(device="cuda:0").manual_seed(0)
     cache.planes.view(torch.int32).random_(generator=gen)
     rng = np.random.default_rng(0)

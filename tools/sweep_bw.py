@@ -42,6 +42,10 @@ def main():
     ap.add_argument("--threads", default="512")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--baselines", default="1,2,0")
+    ap.add_argument("--paths", default="lsu")
+    ap.add_argument("--pieces", default="16384")
+    ap.add_argument("--stages", default="4")
+    ap.add_argument("--no-duplex", action="store_true")
     args = ap.parse_args()
     geo = PRESETS[args.model]
     cache = PagedKVCache(geo, args.pool, device="cuda:0")
@@ -55,13 +59,23 @@ def main():
     for g in [int(x) for x in args.groups.split(",")]:
         ops = orc.random_runs(rng, args.blocks, g, args.pool, args.pool)
         for d in ("out", "in"):
-            for t in [int(x) for x in args.threads.split(",")]:
+            combos = []
+            for path in args.paths.split(","):
+                if path == "lsu":
+                    combos += [(path, 0, 0, t) for t in [int(x) for x in args.threads.split(",")]]
+                else:
+                    combos += [(path, pb, st, 32) for pb in [int(x) for x in args.pieces.split(",")]
+                               for st in [int(x) for x in args.stages.split(",")]
+                               if pb * st <= 227 * 1024]
+            for path, pb, st, t in combos:
+                dp.set_path(d, path, pb, st)
                 for c in [int(x) for x in args.ctas.split(",")]:
-                    dp.set_launch(d, c, t)
+                    dp.set_launch(d, c, t if path == "lsu" else 0)
                     sec = timed(lambda: dp.swap(d, ops, stream=s), s, args.reps)
-                    res.append(dict(group=g, dir=d, impl="kernel", ctas=c, threads=t,
-                                    gbs=nbytes / sec / 1e9))
+                    res.append(dict(group=g, dir=d, impl="kernel", path=path, piece=pb, stages=st,
+                                    ctas=c, threads=t, gbs=nbytes / sec / 1e9))
                     print(json.dumps(res[-1]), flush=True)
+            dp.set_path(d, "lsu")
             for mode in [int(x) for x in args.baselines.split(",") if x]:
                 if mode == 0 and g > 16:
                     continue
@@ -69,6 +83,11 @@ def main():
                 res.append(dict(group=g, dir=d, impl=["ce_per_block", "ce_per_run", "ce_batch"][mode],
                                 gbs=nbytes / sec / 1e9))
                 print(json.dumps(res[-1]), flush=True)
+    if args.no_duplex:
+        os.makedirs("gpurun_out", exist_ok=True)
+        with open("gpurun_out/sweep_bw.json", "w") as f:
+            json.dump(res, f, indent=1)
+        return
     # duplex: out and in concurrently on two streams
     s2 = torch.cuda.Stream()
     ops = orc.random_runs(rng, args.blocks // 2, 16, args.pool // 2, args.pool // 2)
