@@ -51,6 +51,7 @@ EXPORTED_SYMBOLS = (
     "kvs_memcpy_baseline",
     "kvs_host_alloc",
     "kvs_host_free",
+    "kvs_stream_read",  # include/kvswap_workload.h
 )
 
 DIRECTIONS = {"out": KVS_DIR_OUT, "in": KVS_DIR_IN}
@@ -111,6 +112,9 @@ def _declare(lib: ctypes.CDLL) -> None:
     ]
     lib.kvs_host_free.restype = c.c_int
     lib.kvs_host_free.argtypes = [c.c_void_p]
+    lib.kvs_stream_read.restype = c.c_int
+    lib.kvs_stream_read.argtypes = [c.c_int, c.c_uint64, c.c_void_p, c.c_size_t, c.c_size_t,
+                                    c.c_int, c.c_void_p]
 
 
 def load(path: Optional[os.PathLike] = None) -> ctypes.CDLL:

@@ -689,3 +689,51 @@ int kvs_host_free(void* host) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Synthetic decode workload (include/kvswap_workload.h): weight streaming.
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void __launch_bounds__(512) kvs_stream_read_kernel(const int4* __restrict__ buf,
+                                                              uint64_t buf_vecs,
+                                                              uint64_t total_vecs,
+                                                              int4* sink) {
+  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint32_t acc = 0;
+  uint64_t i = tid;
+  // 4 independent 16-B loads in flight per thread.
+  for (; i + 3 * step < total_vecs; i += 4 * step) {
+    int4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = ld_stream(buf + (i + j * step) % buf_vecs);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc ^= v[j].x ^ v[j].y ^ v[j].z ^ v[j].w;
+  }
+  for (; i < total_vecs; i += step) {
+    const int4 v = ld_stream(buf + i % buf_vecs);
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9E3779B9u) sink->x = static_cast<int>(acc);  // practically never
+}
+
+}  // namespace
+
+extern "C" int kvs_stream_read(int device, uint64_t stream, const void* buf, size_t buf_bytes,
+                               size_t bytes, int ctas, void* sink) {
+  if (buf == nullptr || sink == nullptr || buf_bytes < 16 || bytes == 0 || ctas < 0 || device < 0)
+    return KVS_ERR_INVALID;
+  if (reinterpret_cast<uintptr_t>(buf) % 16 || reinterpret_cast<uintptr_t>(sink) % 16)
+    return KVS_ERR_ALIGN;
+  int rc = cuda_rc(cudaSetDevice(device));
+  if (rc) return rc;
+  if (ctas == 0) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    ctas = 2 * sms;
+  }
+  kvs_stream_read_kernel<<<ctas, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      static_cast<const int4*>(buf), buf_bytes / 16, bytes / 16, static_cast<int4*>(sink));
+  return cuda_rc(cudaGetLastError());
+}

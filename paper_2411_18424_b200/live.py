@@ -1,0 +1,283 @@
+"""Live mode: the engine loop driven by real GPU time.
+
+Replay mode (engine.py) reproduces the reference's decisions on its
+simulated clock.  Live mode keeps every decision *rule* of the reference
+(same scheduler, allocator, reuse store, adaptive sync/async) but lets the
+B200 decide *when* things happen:
+
+* the clock is wall time of this process (idle gaps between arrivals are
+  skipped, as the reference's loop does at engine.py:366-371);
+* a swap-in completes when its kernel's CUDA event completes
+  (engine.py:376-384 step 1 made real), not at a modeled exec_done;
+* an iteration's compute is a real HBM-streaming kernel on a high-priority
+  stream, sized to the reference's iteration_time (costmodel.py:74-82), so
+  swap kernels and "decode" contend for SMs / L2 / HBM like in serving;
+* conflicts (grants over blocks a D2H is still reading, engine.py:411-414)
+  and sync swap-ins (engine.py:436-446) become real stream waits whose cost
+  lands in the measured iteration time.
+
+Reported: P50/P95/P99 TTFT, P99/P99.9 TBT (real microseconds), swap GB/s
+while serving, and swap-induced decode stall = decode-kernel time with
+concurrent swaps / the same kernel alone - 1.  Decisions legitimately
+diverge from replay (SURVEY §0 finding 6); correctness is the byte check.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+from typing import Optional
+
+import torch
+
+from . import _lib
+from .costmodel import TransferParams, iteration_time
+from .core import elapsed
+from .engine import (EFFICIENCY_INTERVAL_ITERS, Engine, EngineConfig, IterationRecord,
+                     MetricsReport, percentile)
+from .swap import decide_mode
+
+LIVE_DEADLOCK_ITERATIONS = 200_000
+
+
+def b200_transfer_params(gbs: float = 51.0) -> TransferParams:
+    """Cost-model stand-in for *predictions* in live mode: one launch per plan
+    (dispatch ~ 1 us/op amortised), measured PCIe rate."""
+    return TransferParams(dispatch_per_op=1, bandwidth=int(gbs * 1000), per_op_latency_floor=2,
+                          sync_batch=8)
+
+
+class DecodeEmulator:
+    """Weight-streaming decode stand-in (include/kvswap_workload.h)."""
+
+    def __init__(self, device, weight_bytes: int = 16 << 30, ctas: int = 0) -> None:
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        self.index = self.device.index if self.device.index is not None else 0
+        self.weights = torch.empty(weight_bytes, dtype=torch.uint8, device=self.device)
+        self.weights.view(torch.int32).random_()
+        self.sink = torch.zeros(4, dtype=torch.int32, device=self.device)
+        self.ctas = ctas
+        self.bytes_per_us = self.calibrate()
+
+    def launch(self, stream, nbytes: int) -> None:
+        rc = self.lib.kvs_stream_read(self.index, int(stream.cuda_stream),
+                                      ctypes.c_void_p(self.weights.data_ptr()),
+                                      self.weights.numel(), int(nbytes), self.ctas,
+                                      ctypes.c_void_p(self.sink.data_ptr()))
+        _lib.check(rc, "kvs_stream_read")
+
+    def launch_us(self, stream, us: float) -> int:
+        nbytes = max(16, int(us * self.bytes_per_us) // 16 * 16)
+        self.launch(stream, nbytes)
+        return nbytes
+
+    def calibrate(self, nbytes: int = 8 << 30) -> float:
+        s = torch.cuda.Stream(device=self.device)
+        self.launch(s, nbytes)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(3):
+            self.launch(s, nbytes)
+        e1.record(s)
+        s.synchronize()
+        return 3 * nbytes / (e0.elapsed_time(e1) * 1e3)
+
+
+@dataclass
+class LiveStats:
+    decode_ms: float = 0.0  # measured decode-kernel time (with concurrent swaps)
+    decode_nominal_ms: float = 0.0  # the same bytes at the calibrated solo rate
+    iterations: int = 0
+    idle_waits: int = 0
+    wall_s: float = 0.0
+
+    @property
+    def decode_stall(self) -> float:
+        if self.decode_nominal_ms <= 0:
+            return 0.0
+        return self.decode_ms / self.decode_nominal_ms - 1.0
+
+
+class LiveEngine(Engine):
+    """Engine whose clock, swap completions and compute are real (one GPU)."""
+
+    def __init__(self, config: EngineConfig, conversations, runtime, decode: DecodeEmulator,
+                 time_scale: float = 1.0) -> None:
+        if runtime is None:
+            raise ValueError("live mode needs a Runtime (real data plane)")
+        super().__init__(config, conversations, runtime=runtime)
+        self.decode = decode
+        self.time_scale = time_scale
+        self.live = LiveStats()
+        self._events: list[tuple] = []
+
+    # -- clock ----------------------------------------------------------------
+
+    def _now(self) -> int:
+        return int((time.perf_counter() - self._t0) * 1e6) + self._skip
+
+    # -- step 1 made real ------------------------------------------------------
+
+    def _collect_live(self) -> bool:
+        moved = False
+        keep = []
+        for f in self.manager.in_flight:
+            if f.transfer is not None and not f.transfer.poll():
+                keep.append(f)
+                continue
+            if f.direction == "out":
+                done = {id(r) for r in f.op_records}
+                self.manager.busy_extents = [r for r in self.manager.busy_extents
+                                             if id(r) not in done]
+            elif self._mark_running(f.request):
+                moved = True
+        self.manager.in_flight = keep
+        return moved
+
+    def _wait_any(self, budget_us: int) -> None:
+        """Nothing to compute: block on the earliest pending transfer (or a tick)."""
+        pending = [f for f in self.manager.in_flight if f.transfer is not None]
+        self.live.idle_waits += 1
+        if pending:
+            pending[0].transfer.event.synchronize()
+        else:
+            time.sleep(budget_us * 1e-6)
+
+    # -- loop --------------------------------------------------------------------
+
+    def run(self) -> MetricsReport:
+        for conv in self.conversations:
+            from .engine import RequestState
+            self.states[conv.id] = RequestState(conv=conv)
+            self._push_future(conv.arrival, conv.id)
+        stalls = {"sync": 0, "conflict": 0, "yield": 0, "recompute": 0}
+        windows: list[tuple[int, float]] = []
+        win_tokens = win_time = win_batch = 0
+        idle = 0
+        first_arrival = self.conversations[0].arrival if self.conversations else 0
+        ex = self.runtime.executor
+        compute = ex.compute
+        self._t0 = time.perf_counter()
+        self._skip = first_arrival
+        wall0 = time.perf_counter()
+
+        while True:
+            self.clock = self._now()
+            self._inject_arrivals()
+            if not self._live_ids():
+                if not self._future:
+                    break
+                nxt = self._future[0][0]
+                if nxt > self.clock:
+                    self._skip += nxt - self.clock
+                continue
+            self.iteration += 1
+            start = self.clock
+            progress = self._collect_live()
+            self._maybe_new_epoch()
+            actions = self._schedule()
+            grants: list[tuple[int, int]] = []
+            self._outs_ready_at = self.clock
+            for req in actions.swap_out:
+                self._preempt(req)
+                progress = True
+            self._grow_decoders(grants)
+            for req in actions.swap_in:
+                progress = self._start_swap_in(req, grants) or progress
+            for req in actions.admit:
+                progress = self._admit(req, grants) or progress
+
+            # Real conflicts: grants over blocks a D2H still reads.
+            self.conflict_count += ex.compute_barrier(grants) if grants else 0
+
+            pending = [f for f in self.manager.in_flight if f.direction == "in"]
+            drain = max((elapsed(f.exec_done, self.clock) for f in pending), default=0)
+            biggest = max((self._footprint_blocks(self.states[f.request]) for f in pending),
+                          default=0)
+            est = iteration_time(sum(self.states[r].pending_input for r in self.qs.running),
+                                 len(self.qs.running), self.infer)
+            decision = decide_mode(drain, biggest, est, self.cfg.sync_threshold_ratio,
+                                   self.cfg.short_request_blocks,
+                                   forced=None if self.mode.adaptive else "sync")
+            if decision.mode == "sync" and pending:
+                self.sync_stall_count += 1
+                for f in pending:
+                    ex.wait_transfer(f.transfer)
+                    self.manager.in_flight.remove(f)
+                    self._mark_running(f.request)
+                progress = True
+            if not self.mode.adaptive:
+                for f in list(self.manager.in_flight):
+                    ex.wait_transfer(f.transfer)
+
+            prefillers, decoders, prefill_tokens, recompute, spans = self._assemble_batch()
+            if not (prefillers or decoders):
+                self._wait_any(self.infer.decode_base)
+                end = self._now()
+                idle = idle + (0 if progress else 1)
+                if idle >= LIVE_DEADLOCK_ITERATIONS:
+                    from .engine import DeadlockError
+                    raise DeadlockError(self._diagnostic_dump())
+                self.clock = end
+                continue
+            nominal_us = iteration_time(prefill_tokens, len(decoders), self.infer) * self.time_scale
+            self.runtime.compute(self, spans)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(compute)
+            nbytes = self.decode.launch_us(compute, nominal_us)
+            e1.record(compute)
+            compute.synchronize()
+            end = self._now()
+            kernel_ms = e0.elapsed_time(e1)
+            self.live.decode_ms += kernel_ms
+            self.live.decode_nominal_ms += nbytes / self.decode.bytes_per_us / 1e3
+            self.live.iterations += 1
+            duration = end - start
+            emitted = self._emit_tokens(prefillers, decoders, end)
+            progress = progress or emitted > 0
+            overhead = max(0, duration - int(kernel_ms * 1e3))
+            stalls["sync"] += overhead  # everything that is not decode compute
+            stalls["recompute"] += recompute * self.infer.prefill_per_token
+            rec = IterationRecord(self.iteration, start, end, prefill_tokens, len(decoders),
+                                  overhead, 0, 0, recompute * self.infer.prefill_per_token,
+                                  emitted)
+            self.records.append(rec)
+            win_tokens += emitted
+            win_time += duration
+            win_batch = max(win_batch, len(prefillers) + len(decoders))
+            if self.iteration % EFFICIENCY_INTERVAL_ITERS == 0 and win_time > 0:
+                windows.append((win_batch, win_tokens * 1e6 / win_time))
+                win_tokens = win_time = win_batch = 0
+            self.clock = end
+            for req in list(self.qs.running):
+                st = self.states[req]
+                if st.remaining_output == 0 and st.pending_input == 0:
+                    self._finish_turn(req)
+                    progress = True
+            idle = 0 if progress else idle + 1
+            if idle >= LIVE_DEADLOCK_ITERATIONS:
+                from .engine import DeadlockError
+                raise DeadlockError(self._diagnostic_dump())
+
+        self.runtime.synchronize()
+        self.live.wall_s = time.perf_counter() - wall0
+        return self._report(stalls, self._efficiencies(windows), first_arrival)
+
+    def latency_summary(self) -> dict:
+        def pct(xs, q):
+            return percentile(xs, q) / 1e3 if xs else None
+        return {
+            "ttft_p50_ms": pct(self.ttft_samples, 0.50),
+            "ttft_p95_ms": pct(self.ttft_samples, 0.95),
+            "ttft_p99_ms": pct(self.ttft_samples, 0.99),
+            "tbt_p50_ms": pct(self.tbt_samples, 0.50),
+            "tbt_p99_ms": pct(self.tbt_samples, 0.99),
+            "tbt_p999_ms": pct(self.tbt_samples, 0.999),
+            "decode_stall_frac": round(self.live.decode_stall, 4),
+            "iterations": self.live.iterations,
+            "idle_waits": self.live.idle_waits,
+            "wall_s": round(self.live.wall_s, 2),
+        }

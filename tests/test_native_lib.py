@@ -10,12 +10,15 @@ import pytest
 
 from paper_2411_18424_b200 import _lib
 
-HEADER = Path(__file__).resolve().parents[1] / "include" / "kvswap.h"
+HEADERS = sorted((Path(__file__).resolve().parents[1] / "include").glob("*.h"))
 
 
 def declared_symbols():
-    text = HEADER.read_text()
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(kvs_\w+)\s*\(", text, re.M)))
+    found = set()
+    for hdr in HEADERS:
+        found |= set(re.findall(r"^\s*(?:const\s+)?[\w\s\*]+?\b(kvs_\w+)\s*\(",
+                                hdr.read_text(), re.M))
+    return sorted(found)
 
 
 def test_header_and_binding_agree():
@@ -63,6 +66,7 @@ def test_argument_validation_without_gpu():
     assert lib.kvs_host_free(ctypes.c_void_p(0x1234)) == _lib.KVS_ERR_INVALID
     h, d = ctypes.c_void_p(), ctypes.c_void_p()
     assert lib.kvs_host_alloc(0, -1, 0, ctypes.byref(h), ctypes.byref(d)) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_stream_read(0, 0, None, 0, 0, 0, None) == _lib.KVS_ERR_INVALID
 
 
 def test_check_maps_codes_to_reference_exceptions():

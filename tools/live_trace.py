@@ -1,0 +1,99 @@
+"""Live-mode multi-turn preemption trace on one B200: P99 TTFT/TBT, swap GB/s
+while serving, swap-induced decode stall.  Compares ablations / copy paths.
+
+python tools/live_trace.py --convs 60 --rate 2 --modes full:kernel,baseline:ce_per_block
+Writes gpurun_out/live_trace.json.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from paper_2411_18424_b200 import config as mconfig  # noqa: E402
+from paper_2411_18424_b200.geometry import PRESETS  # noqa: E402
+from paper_2411_18424_b200.live import DecodeEmulator, LiveEngine, b200_transfer_params  # noqa: E402
+from paper_2411_18424_b200.runtime import Runtime  # noqa: E402
+from paper_2411_18424_b200.workload import generate  # noqa: E402
+
+
+def run_one(args, mode, impl, decode, geo):
+    doc = {
+        "ablation": mode,
+        "block": {"bytes_per_block": geo.block_bytes},
+        "gpu_pool": {"total_blocks": args.gpu_blocks},
+        "cpu_pool": {"total_blocks": args.cpu_blocks},
+        "workload": {"num_conversations": args.convs, "arrival_rate_per_s": args.rate,
+                     "think_time_mean_s": args.think},
+        "trace": {"pattern": args.pattern, "frequency": args.freq},
+    }
+    cfg, wl, _ = mconfig.build(doc)
+    cfg = type(cfg)(**{**cfg.__dict__, "transfer": b200_transfer_params(args.pcie_gbs)})
+    rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, copy_impl=impl,
+                 verify=args.verify, timing=True)
+    eng = LiveEngine(cfg, generate(wl), rt, decode)
+    t0 = time.perf_counter()
+    rep = eng.run()
+    wall = time.perf_counter() - t0
+    lat = eng.latency_summary()
+    st = rt.stats()
+    # swap throughput while serving: bytes / summed per-transfer device time
+    ex = rt.executor
+    secs = {"out": 0.0, "in": 0.0}
+    nbytes = {"out": 0, "in": 0}
+    for r in ex.history:
+        if r.start_event is not None and r.nbytes:
+            secs[r.direction] += r.start_event.elapsed_time(r.event) * 1e-3
+            nbytes[r.direction] += r.nbytes + r.refresh_bytes
+    out = {
+        "mode": mode, "copy_impl": impl, "wall_s": round(wall, 2),
+        "latency": lat,
+        "report": {k: v for k, v in rep.to_dict().items() if k != "granularity_histogram"},
+        "swap": {d: {"bytes": nbytes[d], "gbs_while_busy": round(nbytes[d] / secs[d] / 1e9, 2)
+                     if secs[d] else None, "transfers": sum(1 for r in ex.history
+                                                             if r.direction == d)}
+                 for d in ("out", "in")},
+        "runtime": st,
+    }
+    rt.close()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="llama3-8b")
+    ap.add_argument("--convs", type=int, default=60)
+    ap.add_argument("--rate", type=float, default=2.0)
+    ap.add_argument("--think", type=float, default=10.0)
+    ap.add_argument("--gpu-blocks", type=int, default=512)
+    ap.add_argument("--cpu-blocks", type=int, default=8192)
+    ap.add_argument("--pattern", default="markov")
+    ap.add_argument("--freq", type=float, default=0.04)
+    ap.add_argument("--pcie-gbs", type=float, default=51.0)
+    ap.add_argument("--modes", default="full:kernel,baseline:ce_per_block")
+    ap.add_argument("--weights-gib", type=int, default=16)
+    ap.add_argument("--verify", action="store_true")
+    ap.add_argument("--out", default="gpurun_out/live_trace.json")
+    args = ap.parse_args()
+    geo = PRESETS[args.model]
+    decode = DecodeEmulator("cuda:0", weight_bytes=args.weights_gib << 30)
+    results = {"decode_calibrated_gbs": round(decode.bytes_per_us / 1e3, 1), "runs": []}
+    for item in args.modes.split(","):
+        mode, impl = item.split(":")
+        res = run_one(args, mode, impl, decode, geo)
+        results["runs"].append(res)
+        print(json.dumps({k: res[k] for k in ("mode", "copy_impl", "wall_s", "latency", "swap")}),
+              flush=True)
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as f:
+        json.dump(results, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
