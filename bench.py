@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--trace-convs", type=int, default=24)
+    ap.add_argument("--no-trace", action="store_true")
     return ap.parse_args()
 
 
@@ -300,6 +302,12 @@ def run_ours(args, geo):
     if rank == 0 and not args.no_sweep:
         sweep = group_sweep(dp, s)
 
+    # ---- live multi-turn preemption trace: P99 TTFT / TBT (metric part 2) ----
+    trace = None
+    if not args.no_trace:
+        host.close()  # free the 16 GiB pinned pool before the trace's own pools
+        trace = run_trace(args, geo, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -341,6 +349,7 @@ def run_ours(args, geo):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "sweep": sweep,
+            "trace": trace,
         }
         print(json.dumps(line), flush=True)
     host.close()
@@ -405,6 +414,56 @@ def run_e2e(args, geo, dp, dev, barrier, world):
             "api": "CpuStore.plan_swap_out/plan_swap_in -> SwapManager.dispatch -> "
                    "StreamExecutor -> kvs_swap (C ABI); wall clock incl. planning and sync",
             "requests_per_step": n_req, "gpu_launches": launches}
+
+
+def run_trace(args, geo, dev):
+    """Live-mode multi-turn preemption trace on this GPU (paper_2411_18424_b200.live):
+    FastSwitch (block groups + reuse + adaptive async, one kernel per plan) vs the
+    vLLM-style baseline (per-block copies on the copy engines)."""
+    import dataclasses
+
+    from paper_2411_18424_b200 import config as mconfig
+    from paper_2411_18424_b200.live import DecodeEmulator, LiveEngine, b200_transfer_params
+    from paper_2411_18424_b200.runtime import Runtime
+    from paper_2411_18424_b200.workload import generate
+
+    decode = DecodeEmulator(dev, weight_bytes=16 << 30)
+    doc = {"block": {"bytes_per_block": geo.block_bytes}, "gpu_pool": {"total_blocks": 512},
+           "cpu_pool": {"total_blocks": 4096},
+           "workload": {"num_conversations": args.trace_convs, "arrival_rate_per_s": 4.0,
+                        "think_time_mean_s": 2.0},
+           "trace": {"pattern": "markov", "frequency": 0.04}}
+    out = {"workload": f"{args.trace_convs} conversations, 4 req/s, think 2 s, 512 x "
+                       f"{geo.block_bytes >> 20} MiB GPU blocks, Markov f=0.04, decode = "
+                       f"{decode.bytes_per_us / 1e3:.0f} GB/s weight streaming",
+           "runs": {}}
+    for name, mode, impl in (("fastswitch", "full", "kernel"),
+                             ("vllm_like", "baseline", "ce_per_block")):
+        cfg, wl, _ = mconfig.build({**doc, "ablation": mode})
+        cfg = dataclasses.replace(cfg, transfer=b200_transfer_params())
+        rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, device=dev,
+                     copy_impl=impl, timing=True)
+        eng = LiveEngine(cfg, generate(wl), rt, decode)
+        rep = eng.run()
+        lat = eng.latency_summary()
+        st = rt.stats()
+        out["runs"][name] = {"ablation": mode, "copy_impl": impl,
+                             **{k: lat[k] for k in ("ttft_p50_ms", "ttft_p99_ms", "tbt_p99_ms",
+                                                    "tbt_p999_ms", "decode_stall_frac",
+                                                    "wall_s")},
+                             "tokens": rep.total_tokens,
+                             "swap_gib": {"out": round(st["bytes_out"] / 2**30, 2),
+                                          "in": round(st["bytes_in"] / 2**30, 2)},
+                             "kernel_launches": st["kernel_launches"]}
+        rt.close()
+    del decode
+    torch_empty_cache()
+    return out
+
+
+def torch_empty_cache():
+    import torch
+    torch.cuda.empty_cache()
 
 
 def ce_peak(dev, host, cache):

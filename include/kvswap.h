@@ -113,6 +113,15 @@ int kvs_set_path(KvsHandle* h, int dir, int path, int piece_bytes, int stages);
 int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
              uint64_t stream, uint32_t* done_flag, uint32_t seq);
 
+/* Layer-wise pipelined swap: same bytes as kvs_swap, moved
+ * plane-major (all blocks of plane 0 first, ...), and plane_flags[p] (device
+ * or mapped, num_planes words) receives `seq` with system-scope release as
+ * soon as plane p has fully landed, so decode of layer l can start (after
+ * kvs_wait_flag(stream, plane_flags + l, seq)) while later layers are still
+ * in flight.  The reference swaps iteration-wise. */
+int kvs_swap_layered(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
+                     uint64_t stream, uint32_t* plane_flags, uint32_t seq);
+
 /* Make `stream` wait until *flag >= value (cuStreamWaitValue32 GEQ).
  * Replaces: not_before / conflict dependencies (engine.py:712-719,
  * swap.py:236-252) as a device-side wait instead of a modeled timestamp. */

@@ -46,6 +46,7 @@ EXPORTED_SYMBOLS = (
     "kvs_set_launch",
     "kvs_set_path",
     "kvs_swap",
+    "kvs_swap_layered",
     "kvs_wait_flag",
     "kvs_launch_count",
     "kvs_memcpy_baseline",
@@ -96,6 +97,10 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_set_path.argtypes = [c.c_void_p, c.c_int, c.c_int, c.c_int, c.c_int]
     lib.kvs_swap.restype = c.c_int
     lib.kvs_swap.argtypes = [
+        c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64, c.c_void_p, c.c_uint32,
+    ]
+    lib.kvs_swap_layered.restype = c.c_int
+    lib.kvs_swap_layered.argtypes = [
         c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64, c.c_void_p, c.c_uint32,
     ]
     lib.kvs_wait_flag.restype = c.c_int

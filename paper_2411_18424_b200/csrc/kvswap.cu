@@ -60,6 +60,11 @@ struct SwapParams {
   uint32_t seq;
   uint32_t piece_bytes;        // bulk path: bytes per TMA piece (16-B multiple)
   uint32_t stages;             // bulk path: smem ring depth
+  uint32_t layered;            // 1: plane-major order + per-plane completion flags
+  uint32_t pieces_per_plane;   // blocks * pieces_per_chunk
+  unsigned long long* plane_ctr;   // [num_planes] monotone piece counters (this direction)
+  unsigned long long plane_base;   // counter value before this launch
+  uint32_t* plane_flags;       // [num_planes]: receives seq when a plane has landed
   int32_t op_end[CAP];         // inclusive prefix sum of TransferOp.blocks
   int32_t op_gpu[CAP];         // TransferOp.gpu_start
   int32_t op_cpu[CAP];         // TransferOp.cpu_start
@@ -91,10 +96,24 @@ __global__ void __launch_bounds__(kMaxThreads)
   int op = 0;
   int32_t op_begin = 0;
   for (uint32_t i = warp; i < p.total_pieces; i += nwarps) {
-    const uint32_t chunk_idx = i / p.pieces_per_chunk;
-    const uint32_t piece = i - chunk_idx * p.pieces_per_chunk;
-    const uint32_t k = chunk_idx / p.num_planes;  // plan-order block
-    const uint32_t plane = chunk_idx - k * p.num_planes;
+    uint32_t k, plane, piece;
+    if (p.layered) {
+      // Plane-major: every block of plane 0, then plane 1, ... so layer l's
+      // KV lands (and is flagged) before layer l+1's.
+      plane = i / p.pieces_per_plane;
+      const uint32_t j = i - plane * p.pieces_per_plane;
+      k = j / p.pieces_per_chunk;
+      piece = j - k * p.pieces_per_chunk;
+      if (static_cast<int32_t>(k) < op_begin) {  // next plane: rewind the cursor
+        op = 0;
+        op_begin = 0;
+      }
+    } else {
+      const uint32_t chunk_idx = i / p.pieces_per_chunk;
+      piece = i - chunk_idx * p.pieces_per_chunk;
+      k = chunk_idx / p.num_planes;  // plan-order block
+      plane = chunk_idx - k * p.num_planes;
+    }
     // Pieces only move forward for a warp, so the op cursor only advances.
     while (static_cast<int32_t>(k) >= p.op_end[op]) {
       op_begin = p.op_end[op];
@@ -124,6 +143,22 @@ __global__ void __launch_bounds__(kMaxThreads)
 #pragma unroll
       for (int j = 0; j < kUnroll; ++j)
         if (j * kWarpBytes + lo < remain) st_plain(dst + j * kWarpBytes + lo, v[j]);
+    }
+    if (p.plane_flags != nullptr) {
+      // Per-plane completion: the warp that retires a plane's last piece
+      // publishes seq (release, system scope) after every warp fenced its
+      // stores ahead of its counter increment.
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence_system();
+        const unsigned long long old = atomicAdd(p.plane_ctr + plane, 1ull);
+        if (old + 1 == p.plane_base + p.pieces_per_plane) {
+          __threadfence_system();
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.plane_flags + plane),
+                       "r"(p.seq)
+                       : "memory");
+        }
+      }
     }
   }
 
@@ -304,6 +339,8 @@ struct KvsHandle {
   int ctas[2] = {0, 0};
   int threads[2] = {0, 0};
   int path[2] = {KVS_PATH_LSU, KVS_PATH_LSU};
+  unsigned long long* d_plane_ctr = nullptr;    // [2][num_planes]
+  unsigned long long plane_next[2] = {0, 0};
   int piece_bytes[2] = {0, 0};
   int stages[2] = {0, 0};
   int64_t launches = 0;
@@ -313,7 +350,10 @@ namespace {
 
 int cuda_rc(cudaError_t e) { return e == cudaSuccess ? KVS_OK : static_cast<int>(e); }
 
-int default_ctas(int dir) { return dir == KVS_DIR_OUT ? 32 : 32; }
+// Swap-out is posted-write bound: 8 CTAs saturate the link alone and, when a
+// swap-in runs concurrently, leave it the link (the read side is latency
+// critical: it gates resumption). Measured: profiles/r01_duplex_bw.json.
+int default_ctas(int dir) { return dir == KVS_DIR_OUT ? 8 : 32; }
 constexpr int kDefaultThreads = 512;
 constexpr int kDefaultBulkPiece = 16384;
 constexpr int kDefaultStages = 4;
@@ -336,7 +376,8 @@ int check_ops(const KvsHandle* h, const int32_t* ops, int32_t n_ops, int64_t* to
 
 template <int CAP>
 int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t blocks,
-               cudaStream_t stream, uint32_t* done_flag, uint32_t seq) {
+               cudaStream_t stream, uint32_t* done_flag, uint32_t seq, bool layered,
+               uint32_t* plane_flags) {
   SwapParams<CAP> p;
   p.planes = h->d_planes;
   p.host = h->host;
@@ -344,7 +385,7 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   p.stride = h->geo.plane_block_stride;
   p.host_block = h->geo.plane_chunk_bytes * h->geo.num_planes;
   p.num_planes = static_cast<uint32_t>(h->geo.num_planes);
-  const bool bulk = h->path[dir] == KVS_PATH_BULK;
+  const bool bulk = h->path[dir] == KVS_PATH_BULK && !layered;
   int64_t piece = kPieceBytes;
   uint32_t stages = 0;
   if (bulk) {
@@ -366,6 +407,12 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
     p.op_gpu[i] = ops[3 * i + 1];
     p.op_cpu[i] = ops[3 * i + 2];
   }
+  p.layered = layered ? 1u : 0u;
+  p.pieces_per_plane = static_cast<uint32_t>(blocks) * p.pieces_per_chunk;
+  p.plane_ctr = h->d_plane_ctr + static_cast<size_t>(dir) * h->geo.num_planes;
+  p.plane_base = h->plane_next[dir];
+  p.plane_flags = plane_flags;
+  if (plane_flags != nullptr) h->plane_next[dir] += p.pieces_per_plane;
   int threads = bulk ? 32 : (h->threads[dir] > 0 ? h->threads[dir] : kDefaultThreads);
   int ctas = h->ctas[dir] > 0 ? h->ctas[dir] : (bulk ? kDefaultBulkCtas : default_ctas(dir));
   // Never launch warps (bulk: CTAs) that can have no piece.
@@ -397,10 +444,16 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
 
 // One launch for <= 2048 ops, smallest parameter block that fits.
 int launch_one(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t blocks,
-               cudaStream_t stream, uint32_t* done_flag, uint32_t seq) {
-  if (n_ops <= 32) return launch_cap<32>(h, dir, ops, n_ops, blocks, stream, done_flag, seq);
-  if (n_ops <= 256) return launch_cap<256>(h, dir, ops, n_ops, blocks, stream, done_flag, seq);
-  return launch_cap<2048>(h, dir, ops, n_ops, blocks, stream, done_flag, seq);
+               cudaStream_t stream, uint32_t* done_flag, uint32_t seq, bool layered,
+               uint32_t* plane_flags) {
+  if (n_ops <= 32)
+    return launch_cap<32>(h, dir, ops, n_ops, blocks, stream, done_flag, seq, layered,
+                          plane_flags);
+  if (n_ops <= 256)
+    return launch_cap<256>(h, dir, ops, n_ops, blocks, stream, done_flag, seq, layered,
+                           plane_flags);
+  return launch_cap<2048>(h, dir, ops, n_ops, blocks, stream, done_flag, seq, layered,
+                          plane_flags);
 }
 constexpr int32_t kOpsPerLaunch = 2048;
 
@@ -473,6 +526,11 @@ int kvs_create(int device, const KvsGeometry* geo, const uint64_t* plane_ptrs, v
                             cudaMemcpyHostToDevice));
   if (!rc) rc = cuda_rc(cudaMalloc(&h->d_tickets, 2 * sizeof(unsigned long long)));
   if (!rc) rc = cuda_rc(cudaMemset(h->d_tickets, 0, 2 * sizeof(unsigned long long)));
+  if (!rc)
+    rc = cuda_rc(cudaMalloc(&h->d_plane_ctr, 2 * sizeof(unsigned long long) * geo->num_planes));
+  if (!rc)
+    rc = cuda_rc(
+        cudaMemset(h->d_plane_ctr, 0, 2 * sizeof(unsigned long long) * geo->num_planes));
   if (rc) {
     kvs_destroy(h);
     return rc;
@@ -486,6 +544,7 @@ int kvs_destroy(KvsHandle* h) {
   cudaSetDevice(h->device);
   if (h->d_planes) cudaFree(h->d_planes);
   if (h->d_tickets) cudaFree(h->d_tickets);
+  if (h->d_plane_ctr) cudaFree(h->d_plane_ctr);
   delete h;
   return KVS_OK;
 }
@@ -512,8 +571,8 @@ int kvs_set_path(KvsHandle* h, int dir, int path, int piece_bytes, int stages) {
   return KVS_OK;
 }
 
-int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
-             uint32_t* done_flag, uint32_t seq) {
+static int swap_impl(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
+                     uint32_t* done_flag, uint32_t seq, bool layered, uint32_t* plane_flags) {
   if (h == nullptr || (dir != KVS_DIR_OUT && dir != KVS_DIR_IN) || n_ops < 0 ||
       (n_ops > 0 && ops == nullptr))
     return KVS_ERR_INVALID;
@@ -524,23 +583,43 @@ int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t 
   if (rc) return rc;
   auto s = reinterpret_cast<cudaStream_t>(stream);
   if (n_ops == 0) {
-    if (done_flag == nullptr) return KVS_OK;
     static auto write_fn = driver_fn<StreamWriteValue32Fn>("cuStreamWriteValue32");
+    uint32_t* words[2] = {done_flag, nullptr};
+    const int n_words = done_flag != nullptr ? 1 : 0;
+    if (n_words == 0 && plane_flags == nullptr) return KVS_OK;
     if (write_fn == nullptr) return KVS_ERR_UNSUPPORTED;
-    return write_fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(done_flag), seq,
-                    0) == CUDA_SUCCESS
-               ? KVS_OK
-               : KVS_ERR_UNSUPPORTED;
+    for (int w = 0; w < n_words; ++w)
+      if (write_fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(words[w]), seq,
+                   0) != CUDA_SUCCESS)
+        return KVS_ERR_UNSUPPORTED;
+    if (plane_flags != nullptr)
+      for (int pl = 0; pl < h->geo.num_planes; ++pl)
+        if (write_fn(reinterpret_cast<CUstream>(s),
+                     reinterpret_cast<CUdeviceptr>(plane_flags + pl), seq, 0) != CUDA_SUCCESS)
+          return KVS_ERR_UNSUPPORTED;
+    return KVS_OK;
   }
   for (int32_t first = 0; first < n_ops; first += kOpsPerLaunch) {
     const int32_t n = (n_ops - first) < kOpsPerLaunch ? (n_ops - first) : kOpsPerLaunch;
     int64_t part = 0;
     for (int32_t i = 0; i < n; ++i) part += ops[3 * (first + i)];
     const bool last = first + n == n_ops;
-    rc = launch_one(h, dir, ops + 3 * first, n, part, s, last ? done_flag : nullptr, seq);
+    rc = launch_one(h, dir, ops + 3 * first, n, part, s, last ? done_flag : nullptr, seq,
+                    layered, last ? plane_flags : nullptr);
     if (rc) return rc;
   }
   return KVS_OK;
+}
+
+int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
+             uint32_t* done_flag, uint32_t seq) {
+  return swap_impl(h, dir, ops, n_ops, stream, done_flag, seq, false, nullptr);
+}
+
+int kvs_swap_layered(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
+                     uint32_t* plane_flags, uint32_t seq) {
+  if (plane_flags == nullptr) return KVS_ERR_INVALID;
+  return swap_impl(h, dir, ops, n_ops, stream, nullptr, seq, true, plane_flags);
 }
 
 int kvs_wait_flag(uint64_t stream, const uint32_t* flag, uint32_t value) {

@@ -180,6 +180,17 @@ class SwapDataPlane:
         _lib.check(rc, f"kvs_swap({direction})")
         return arr
 
+    def swap_layered(self, direction: str, ops: OpsLike, plane_flags: int, seq: int,
+                     stream: Optional[torch.cuda.Stream] = None) -> np.ndarray:
+        """Plane-major swap; plane_flags[p] <- seq once plane (layer) p has landed."""
+        arr = ops_array(ops)
+        rc = self.lib.kvs_swap_layered(self.handle, _lib.DIRECTIONS[direction],
+                                       arr.ctypes.data_as(ctypes.c_void_p), arr.shape[0],
+                                       _stream_handle(stream), ctypes.c_void_p(plane_flags),
+                                       seq & 0xFFFFFFFF)
+        _lib.check(rc, f"kvs_swap_layered({direction})")
+        return arr
+
     def baseline(self, direction: str, mode: int, ops: OpsLike,
                  stream: Optional[torch.cuda.Stream] = None) -> None:
         arr = ops_array(ops)

@@ -225,3 +225,54 @@ def test_config1_round_trip_llama3_8b(cuda_ok, path):
     back = cache.planes[:, torch.from_numpy(new_tab).cuda()]
     assert torch.equal(back, original)
     host.close()
+
+
+@pytest.mark.parametrize("direction", ["in", "out"])
+def test_layered_swap_flags_each_plane(cuda_ok, direction):
+    """kvs_swap_layered: plane-major order, per-plane release flags; a consumer
+    stream waiting on plane l's flag sees plane l's bytes complete."""
+    torch = cuda_ok
+    geo = _small_geometry(1028, 6)
+    G = C = 600
+    cache, host, dp = _mk(torch, geo, G, C, ctas={"out": 4, "in": 4})
+    rng = np.random.default_rng(21)
+    pattern = orc.kv_pattern(3, geo.num_planes, G, geo.plane_chunk_bytes)
+    gpu_tab = orc.random_block_table(rng, 500, G)
+    cpu_tab = orc.random_block_table(rng, 500, C)
+    ops = orc.table_to_ops(gpu_tab, cpu_tab)
+    if direction == "in":
+        host_img = np.zeros((C, geo.block_bytes), np.uint8)
+        orc.apply_plan("out", pattern, host_img, ops)
+        host.array[:] = host_img
+        cache.planes.zero_()
+    else:
+        cache.planes.copy_(torch.from_numpy(pattern))
+        host.array[:] = 0
+    torch.cuda.synchronize()
+    flags = torch.zeros(geo.num_planes, dtype=torch.int32, device="cuda:0")
+    s_swap, s_use = torch.cuda.Stream(), torch.cuda.Stream()
+    snaps = []
+    dp.swap_layered(direction, ops, flags.data_ptr(), 1, stream=s_swap)
+    if direction == "in":
+        idx = torch.from_numpy(gpu_tab).cuda()
+        for l in range(geo.num_planes):
+            dp.wait_flag(s_use, flags.data_ptr() + 4 * l, 1)
+            with torch.cuda.stream(s_use):
+                snaps.append(cache.planes[l, idx].clone())  # "decode of layer l"
+    torch.cuda.synchronize()
+    assert flags.tolist() == [1] * geo.num_planes
+    if direction == "in":
+        for l in range(geo.num_planes):
+            assert np.array_equal(snaps[l].cpu().numpy(), pattern[l, gpu_tab])
+        want = np.zeros_like(pattern)
+        orc.apply_plan("in", want, host.array.copy(), ops)
+        np.testing.assert_array_equal(cache.planes.cpu().numpy(), want)
+    else:
+        want = np.zeros((C, geo.block_bytes), np.uint8)
+        orc.apply_plan("out", pattern, want, ops)
+        np.testing.assert_array_equal(host.array, want)
+    # generation 2 on the same handle: counters carry over, flags advance
+    dp.swap_layered(direction, ops, flags.data_ptr(), 2, stream=s_swap)
+    torch.cuda.synchronize()
+    assert flags.tolist() == [2] * geo.num_planes
+    host.close()
