@@ -293,6 +293,8 @@ def run_ours(args, geo):
 
     # ---- e2e: public API (control plane + dispatch) with host round trip ----
     e2e = run_e2e(args, geo, dp, dev, barrier, world)
+    dp.set_launch("out", args.ctas, 0)
+    dp.set_launch("in", args.ctas, 0)
 
     # ---- copy-engine peak on this box (roofline context) ----
     ce = ce_peak(dev, host, cache) if rank == 0 else None
@@ -366,7 +368,7 @@ def run_e2e(args, geo, dp, dev, barrier, world):
     from paper_2411_18424_b200.cpu_store import CpuStore
     from paper_2411_18424_b200.swap import StreamExecutor, SwapManager
 
-    ex = StreamExecutor(dp)
+    ex = StreamExecutor(dp, duplex_policy="throughput")  # bulk round trip: max combined GB/s
     mgr = SwapManager(TransferParams(), bytes_per_block=geo.block_bytes, executor=ex)
     store = CpuStore(POOL_BLOCKS, reuse_enabled=True)
     n_req, per = 64, PLAN_BLOCKS // 64

@@ -65,6 +65,8 @@ struct SwapParams {
   unsigned long long* plane_ctr;   // [num_planes] monotone piece counters (this direction)
   unsigned long long plane_base;   // counter value before this launch
   uint32_t* plane_flags;       // [num_planes]: receives seq when a plane has landed
+  uint32_t* op_ctr;            // [n_ops] piece counters, zeroed before the launch
+  uint32_t* op_flags;          // [n_ops]: receives seq when a TransferOp has landed
   int32_t op_end[CAP];         // inclusive prefix sum of TransferOp.blocks
   int32_t op_gpu[CAP];         // TransferOp.gpu_start
   int32_t op_cpu[CAP];         // TransferOp.cpu_start
@@ -144,19 +146,31 @@ __global__ void __launch_bounds__(kMaxThreads)
       for (int j = 0; j < kUnroll; ++j)
         if (j * kWarpBytes + lo < remain) st_plain(dst + j * kWarpBytes + lo, v[j]);
     }
-    if (p.plane_flags != nullptr) {
-      // Per-plane completion: the warp that retires a plane's last piece
-      // publishes seq (release, system scope) after every warp fenced its
-      // stores ahead of its counter increment.
+    if (p.plane_flags != nullptr || p.op_flags != nullptr) {
+      // Fine-grained completion: the warp that retires the last piece of a
+      // plane (layered) or of a TransferOp publishes seq (release, system
+      // scope); every warp fences its stores ahead of its counter increment.
       __syncwarp();
       if (lane == 0) {
         __threadfence_system();
-        const unsigned long long old = atomicAdd(p.plane_ctr + plane, 1ull);
-        if (old + 1 == p.plane_base + p.pieces_per_plane) {
-          __threadfence_system();
-          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.plane_flags + plane),
-                       "r"(p.seq)
-                       : "memory");
+        if (p.plane_flags != nullptr) {
+          const unsigned long long old = atomicAdd(p.plane_ctr + plane, 1ull);
+          if (old + 1 == p.plane_base + p.pieces_per_plane) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.plane_flags + plane),
+                         "r"(p.seq)
+                         : "memory");
+          }
+        }
+        if (p.op_flags != nullptr) {
+          const uint32_t want = static_cast<uint32_t>(p.op_end[op] - op_begin) * p.num_planes *
+                                p.pieces_per_chunk;
+          if (atomicAdd(p.op_ctr + op, 1u) + 1 == want) {
+            __threadfence_system();
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.op_flags + op),
+                         "r"(p.seq)
+                         : "memory");
+          }
         }
       }
     }

@@ -111,7 +111,9 @@ class LiveEngine(Engine):
         self.decode = decode
         self.time_scale = time_scale
         self.live = LiveStats()
-        self._events: list[tuple] = []
+        # per computing iteration: (duration_us, cpu_us, wait_ms, kernel_ms,
+        #                           synced, conflict_waits, n_prefill, n_decode)
+        self._trace: list[tuple] = []
 
     # -- clock ----------------------------------------------------------------
 
@@ -175,6 +177,7 @@ class LiveEngine(Engine):
                 continue
             self.iteration += 1
             start = self.clock
+            t_iter = time.perf_counter()
             progress = self._collect_live()
             self._maybe_new_epoch()
             actions = self._schedule()
@@ -190,7 +193,10 @@ class LiveEngine(Engine):
                 progress = self._admit(req, grants) or progress
 
             # Real conflicts: grants over blocks a D2H still reads.
-            self.conflict_count += ex.compute_barrier(grants) if grants else 0
+            e_pre = torch.cuda.Event(enable_timing=True)
+            e_pre.record(compute)  # GPU-side waits of this iteration start here
+            conf_now = ex.compute_barrier(grants) if grants else 0
+            self.conflict_count += conf_now
 
             pending = [f for f in self.manager.in_flight if f.direction == "in"]
             drain = max((elapsed(f.exec_done, self.clock) for f in pending), default=0)
@@ -223,6 +229,7 @@ class LiveEngine(Engine):
                 self.clock = end
                 continue
             nominal_us = iteration_time(prefill_tokens, len(decoders), self.infer) * self.time_scale
+            t_cpu = time.perf_counter()
             self.runtime.compute(self, spans)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
@@ -232,6 +239,10 @@ class LiveEngine(Engine):
             compute.synchronize()
             end = self._now()
             kernel_ms = e0.elapsed_time(e1)
+            self._trace.append((end - start, int((t_cpu - t_iter) * 1e6), e_pre.elapsed_time(e0),
+                                kernel_ms, decision.mode == "sync" and bool(pending),
+                                conf_now, len(prefillers),
+                                len(decoders)))
             self.live.decode_ms += kernel_ms
             self.live.decode_nominal_ms += nbytes / self.decode.bytes_per_us / 1e3
             self.live.iterations += 1
@@ -266,6 +277,27 @@ class LiveEngine(Engine):
         self.live.wall_s = time.perf_counter() - wall0
         return self._report(stalls, self._efficiencies(windows), first_arrival)
 
+    def spike_breakdown(self, q: float = 0.99) -> dict:
+        """Where the slowest (>= q quantile) iterations spend their time."""
+        if not self._trace:
+            return {}
+        durs = sorted(t[0] for t in self._trace)
+        cut = durs[min(len(durs) - 1, int(q * len(durs)))]
+        slow = [t for t in self._trace if t[0] >= cut]
+        n = len(slow)
+        return {
+            "quantile": q, "threshold_ms": cut / 1e3, "iterations": n,
+            "mean_ms": sum(t[0] for t in slow) / n / 1e3,
+            "mean_cpu_ms": sum(t[1] for t in slow) / n / 1e3,
+            "mean_gpu_wait_ms": sum(t[2] for t in slow) / n,
+            "mean_decode_kernel_ms": sum(t[3] for t in slow) / n,
+            "frac_with_sync_swap_in": sum(1 for t in slow if t[4]) / n,
+            "frac_with_conflict_wait": sum(1 for t in slow if t[5]) / n,
+            "mean_prefill_requests": sum(t[6] for t in slow) / n,
+            "overall_mean_ms": sum(durs) / len(durs) / 1e3,
+            "overall_mean_cpu_ms": sum(t[1] for t in self._trace) / len(self._trace) / 1e3,
+        }
+
     def latency_summary(self) -> dict:
         def pct(xs, q):
             return percentile(xs, q) / 1e3 if xs else None
@@ -280,4 +312,5 @@ class LiveEngine(Engine):
             "iterations": self.live.iterations,
             "idle_waits": self.live.idle_waits,
             "wall_s": round(self.live.wall_s, 2),
+            "slow_iterations": self.spike_breakdown(),
         }

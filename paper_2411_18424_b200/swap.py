@@ -166,12 +166,20 @@ class TransferRecord:
 
 COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 
+# Swap-kernel CTAs per direction.  Both directions alone saturate PCIe with
+# >= 4-8 CTAs; they differ when swap-out and swap-in overlap
+# (profiles/r01_duplex_bw.json):
+#   latency    — swap-in keeps ~50 GB/s, swap-out takes what is left (serving:
+#                resumption gates TTFT, swap-out only gates host-space reuse);
+#   throughput — balanced, highest combined GB/s (bulk migration).
+DUPLEX_POLICIES = {"latency": {"out": 8, "in": 32}, "throughput": {"out": 32, "in": 32}}
+
 
 class StreamExecutor:
     """Real streams + event hazards around one SwapDataPlane (one rank)."""
 
     def __init__(self, dataplane, compute_stream=None, copy_impl: str = "kernel",
-                 timing: bool = False) -> None:
+                 timing: bool = False, duplex_policy: str = "latency") -> None:
         import torch
 
         if copy_impl not in COPY_IMPLS:
@@ -179,8 +187,6 @@ class StreamExecutor:
         self.torch = torch
         self.dp = dataplane
         dev = dataplane.cache.device
-        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") \
-            else (0, -1)
         self.streams = {
             "out": torch.cuda.Stream(device=dev, priority=0),
             "in": torch.cuda.Stream(device=dev, priority=0),
@@ -195,6 +201,14 @@ class StreamExecutor:
         self.refresh_bytes = 0
         self.launches = 0
         self.block_bytes = dataplane.geometry.block_bytes
+        self.set_duplex_policy(duplex_policy)
+
+    def set_duplex_policy(self, policy: str) -> None:
+        if policy not in DUPLEX_POLICIES:
+            raise ValueError(f"duplex policy must be one of {sorted(DUPLEX_POLICIES)}")
+        for direction, ctas in DUPLEX_POLICIES[policy].items():
+            self.dp.set_launch(direction, ctas, 0)
+        self.duplex_policy = policy
 
     def _prune(self) -> None:
         self.pending = [r for r in self.pending if not r.poll()]
