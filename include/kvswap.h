@@ -122,6 +122,16 @@ int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
 int kvs_swap_layered(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
                      uint64_t stream, uint32_t* plane_flags, uint32_t seq);
 
+/* Op-granular completion (SURVEY §7 hard part 4): same bytes as kvs_swap;
+ * op_flags[i] (device or mapped, n_ops words) receives `seq` with
+ * system-scope release once TransferOp i has fully landed, and done_flag
+ * (optional) once the whole plan has.  A conflicting grant or swap-in then
+ * waits for the blocking op only, as the reference resolves conflicts per op
+ * (swap.py:236-252, engine.py:712-719), not for the whole plan.  Counters are
+ * per handle and direction: issue one direction's calls on one stream. */
+int kvs_swap_ops(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
+                 uint64_t stream, uint32_t* op_flags, uint32_t* done_flag, uint32_t seq);
+
 /* Make `stream` wait until *flag >= value (cuStreamWaitValue32 GEQ).
  * Replaces: not_before / conflict dependencies (engine.py:712-719,
  * swap.py:236-252) as a device-side wait instead of a modeled timestamp. */

@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = (
     "kvs_set_path",
     "kvs_swap",
     "kvs_swap_layered",
+    "kvs_swap_ops",
     "kvs_wait_flag",
     "kvs_launch_count",
     "kvs_memcpy_baseline",
@@ -102,6 +103,11 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_swap_layered.restype = c.c_int
     lib.kvs_swap_layered.argtypes = [
         c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64, c.c_void_p, c.c_uint32,
+    ]
+    lib.kvs_swap_ops.restype = c.c_int
+    lib.kvs_swap_ops.argtypes = [
+        c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64, c.c_void_p, c.c_void_p,
+        c.c_uint32,
     ]
     lib.kvs_wait_flag.restype = c.c_int
     lib.kvs_wait_flag.argtypes = [c.c_uint64, c.c_void_p, c.c_uint32]

@@ -354,6 +354,7 @@ struct KvsHandle {
   int threads[2] = {0, 0};
   int path[2] = {KVS_PATH_LSU, KVS_PATH_LSU};
   unsigned long long* d_plane_ctr = nullptr;    // [2][num_planes]
+  uint32_t* d_op_ctr = nullptr;                 // [2][kOpsPerLaunchMax]
   unsigned long long plane_next[2] = {0, 0};
   int piece_bytes[2] = {0, 0};
   int stages[2] = {0, 0};
@@ -368,6 +369,7 @@ int cuda_rc(cudaError_t e) { return e == cudaSuccess ? KVS_OK : static_cast<int>
 // swap-in runs concurrently, leave it the link (the read side is latency
 // critical: it gates resumption). Measured: profiles/r01_duplex_bw.json.
 int default_ctas(int dir) { return dir == KVS_DIR_OUT ? 8 : 32; }
+constexpr int32_t kOpsPerLaunchMax = 2048;
 constexpr int kDefaultThreads = 512;
 constexpr int kDefaultBulkPiece = 16384;
 constexpr int kDefaultStages = 4;
@@ -388,10 +390,18 @@ int check_ops(const KvsHandle* h, const int32_t* ops, int32_t n_ops, int64_t* to
   return KVS_OK;
 }
 
+// Completion signalling requested for one launch.
+struct LaunchOpts {
+  uint32_t* done_flag = nullptr;    // whole launch landed
+  uint32_t* plane_flags = nullptr;  // per plane (implies plane-major order)
+  uint32_t* op_flags = nullptr;     // per TransferOp of this launch
+  uint32_t seq = 0;
+  bool layered = false;
+};
+
 template <int CAP>
 int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t blocks,
-               cudaStream_t stream, uint32_t* done_flag, uint32_t seq, bool layered,
-               uint32_t* plane_flags) {
+               cudaStream_t stream, const LaunchOpts& o) {
   SwapParams<CAP> p;
   p.planes = h->d_planes;
   p.host = h->host;
@@ -399,7 +409,8 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   p.stride = h->geo.plane_block_stride;
   p.host_block = h->geo.plane_chunk_bytes * h->geo.num_planes;
   p.num_planes = static_cast<uint32_t>(h->geo.num_planes);
-  const bool bulk = h->path[dir] == KVS_PATH_BULK && !layered;
+  // The bulk (TMA) path signals only whole-launch completion.
+  const bool bulk = h->path[dir] == KVS_PATH_BULK && !o.layered && o.op_flags == nullptr;
   int64_t piece = kPieceBytes;
   uint32_t stages = 0;
   if (bulk) {
@@ -421,12 +432,20 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
     p.op_gpu[i] = ops[3 * i + 1];
     p.op_cpu[i] = ops[3 * i + 2];
   }
-  p.layered = layered ? 1u : 0u;
+  p.layered = o.layered ? 1u : 0u;
   p.pieces_per_plane = static_cast<uint32_t>(blocks) * p.pieces_per_chunk;
   p.plane_ctr = h->d_plane_ctr + static_cast<size_t>(dir) * h->geo.num_planes;
   p.plane_base = h->plane_next[dir];
-  p.plane_flags = plane_flags;
-  if (plane_flags != nullptr) h->plane_next[dir] += p.pieces_per_plane;
+  p.plane_flags = o.plane_flags;
+  if (o.plane_flags != nullptr) h->plane_next[dir] += p.pieces_per_plane;
+  p.op_ctr = h->d_op_ctr + static_cast<size_t>(dir) * kOpsPerLaunchMax;
+  p.op_flags = o.op_flags;
+  if (o.op_flags != nullptr) {
+    // Same stream as the kernel: ordered before it, and after the previous
+    // launch of this direction that used the counters.
+    int rc = cuda_rc(cudaMemsetAsync(p.op_ctr, 0, sizeof(uint32_t) * n_ops, stream));
+    if (rc) return rc;
+  }
   int threads = bulk ? 32 : (h->threads[dir] > 0 ? h->threads[dir] : kDefaultThreads);
   int ctas = h->ctas[dir] > 0 ? h->ctas[dir] : (bulk ? kDefaultBulkCtas : default_ctas(dir));
   // Never launch warps (bulk: CTAs) that can have no piece.
@@ -434,11 +453,11 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   const uint64_t max_ctas = (pieces + units_per_cta - 1) / units_per_cta;
   if (static_cast<uint64_t>(ctas) > max_ctas) ctas = static_cast<int>(max_ctas);
   if (ctas < 1) ctas = 1;
-  p.done_flag = done_flag;
+  p.done_flag = o.done_flag;
   p.ticket = h->d_tickets + dir;
   p.ticket_base = h->ticket_next[dir];
-  p.seq = seq;
-  if (done_flag != nullptr) h->ticket_next[dir] += static_cast<unsigned long long>(ctas);
+  p.seq = o.seq;
+  if (o.done_flag != nullptr) h->ticket_next[dir] += static_cast<unsigned long long>(ctas);
   if (bulk) {
     const size_t smem = static_cast<size_t>(stages) * static_cast<size_t>(piece);
     auto kern = dir == KVS_DIR_OUT ? kvs_swap_bulk_kernel<KVS_DIR_OUT, CAP>
@@ -458,18 +477,12 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
 
 // One launch for <= 2048 ops, smallest parameter block that fits.
 int launch_one(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t blocks,
-               cudaStream_t stream, uint32_t* done_flag, uint32_t seq, bool layered,
-               uint32_t* plane_flags) {
-  if (n_ops <= 32)
-    return launch_cap<32>(h, dir, ops, n_ops, blocks, stream, done_flag, seq, layered,
-                          plane_flags);
-  if (n_ops <= 256)
-    return launch_cap<256>(h, dir, ops, n_ops, blocks, stream, done_flag, seq, layered,
-                           plane_flags);
-  return launch_cap<2048>(h, dir, ops, n_ops, blocks, stream, done_flag, seq, layered,
-                          plane_flags);
+               cudaStream_t stream, const LaunchOpts& o) {
+  if (n_ops <= 32) return launch_cap<32>(h, dir, ops, n_ops, blocks, stream, o);
+  if (n_ops <= 256) return launch_cap<256>(h, dir, ops, n_ops, blocks, stream, o);
+  return launch_cap<2048>(h, dir, ops, n_ops, blocks, stream, o);
 }
-constexpr int32_t kOpsPerLaunch = 2048;
+constexpr int32_t kOpsPerLaunch = kOpsPerLaunchMax;
 
 using StreamWaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using StreamWriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
@@ -545,6 +558,7 @@ int kvs_create(int device, const KvsGeometry* geo, const uint64_t* plane_ptrs, v
   if (!rc)
     rc = cuda_rc(
         cudaMemset(h->d_plane_ctr, 0, 2 * sizeof(unsigned long long) * geo->num_planes));
+  if (!rc) rc = cuda_rc(cudaMalloc(&h->d_op_ctr, 2 * sizeof(uint32_t) * kOpsPerLaunchMax));
   if (rc) {
     kvs_destroy(h);
     return rc;
@@ -559,6 +573,7 @@ int kvs_destroy(KvsHandle* h) {
   if (h->d_planes) cudaFree(h->d_planes);
   if (h->d_tickets) cudaFree(h->d_tickets);
   if (h->d_plane_ctr) cudaFree(h->d_plane_ctr);
+  if (h->d_op_ctr) cudaFree(h->d_op_ctr);
   delete h;
   return KVS_OK;
 }
@@ -586,7 +601,7 @@ int kvs_set_path(KvsHandle* h, int dir, int path, int piece_bytes, int stages) {
 }
 
 static int swap_impl(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
-                     uint32_t* done_flag, uint32_t seq, bool layered, uint32_t* plane_flags) {
+                     const LaunchOpts& o) {
   if (h == nullptr || (dir != KVS_DIR_OUT && dir != KVS_DIR_IN) || n_ops < 0 ||
       (n_ops > 0 && ops == nullptr))
     return KVS_ERR_INVALID;
@@ -597,20 +612,18 @@ static int swap_impl(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, u
   if (rc) return rc;
   auto s = reinterpret_cast<cudaStream_t>(stream);
   if (n_ops == 0) {
+    // Nothing to move: still publish the requested completion words in order.
+    if (o.done_flag == nullptr && o.plane_flags == nullptr) return KVS_OK;
     static auto write_fn = driver_fn<StreamWriteValue32Fn>("cuStreamWriteValue32");
-    uint32_t* words[2] = {done_flag, nullptr};
-    const int n_words = done_flag != nullptr ? 1 : 0;
-    if (n_words == 0 && plane_flags == nullptr) return KVS_OK;
     if (write_fn == nullptr) return KVS_ERR_UNSUPPORTED;
-    for (int w = 0; w < n_words; ++w)
-      if (write_fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(words[w]), seq,
-                   0) != CUDA_SUCCESS)
-        return KVS_ERR_UNSUPPORTED;
-    if (plane_flags != nullptr)
+    auto put = [&](uint32_t* w) {
+      return write_fn(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(w), o.seq,
+                      0) == CUDA_SUCCESS;
+    };
+    if (o.done_flag != nullptr && !put(o.done_flag)) return KVS_ERR_UNSUPPORTED;
+    if (o.plane_flags != nullptr)
       for (int pl = 0; pl < h->geo.num_planes; ++pl)
-        if (write_fn(reinterpret_cast<CUstream>(s),
-                     reinterpret_cast<CUdeviceptr>(plane_flags + pl), seq, 0) != CUDA_SUCCESS)
-          return KVS_ERR_UNSUPPORTED;
+        if (!put(o.plane_flags + pl)) return KVS_ERR_UNSUPPORTED;
     return KVS_OK;
   }
   for (int32_t first = 0; first < n_ops; first += kOpsPerLaunch) {
@@ -618,8 +631,13 @@ static int swap_impl(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, u
     int64_t part = 0;
     for (int32_t i = 0; i < n; ++i) part += ops[3 * (first + i)];
     const bool last = first + n == n_ops;
-    rc = launch_one(h, dir, ops + 3 * first, n, part, s, last ? done_flag : nullptr, seq,
-                    layered, last ? plane_flags : nullptr);
+    LaunchOpts lo = o;
+    if (!last) {  // whole-launch and per-plane words belong to the final launch
+      lo.done_flag = nullptr;
+      lo.plane_flags = nullptr;
+    }
+    if (o.op_flags != nullptr) lo.op_flags = o.op_flags + first;
+    rc = launch_one(h, dir, ops + 3 * first, n, part, s, lo);
     if (rc) return rc;
   }
   return KVS_OK;
@@ -627,13 +645,30 @@ static int swap_impl(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, u
 
 int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
              uint32_t* done_flag, uint32_t seq) {
-  return swap_impl(h, dir, ops, n_ops, stream, done_flag, seq, false, nullptr);
+  LaunchOpts o;
+  o.done_flag = done_flag;
+  o.seq = seq;
+  return swap_impl(h, dir, ops, n_ops, stream, o);
 }
 
 int kvs_swap_layered(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
                      uint32_t* plane_flags, uint32_t seq) {
   if (plane_flags == nullptr) return KVS_ERR_INVALID;
-  return swap_impl(h, dir, ops, n_ops, stream, nullptr, seq, true, plane_flags);
+  LaunchOpts o;
+  o.plane_flags = plane_flags;
+  o.layered = true;
+  o.seq = seq;
+  return swap_impl(h, dir, ops, n_ops, stream, o);
+}
+
+int kvs_swap_ops(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
+                 uint32_t* op_flags, uint32_t* done_flag, uint32_t seq) {
+  if (op_flags == nullptr) return KVS_ERR_INVALID;
+  LaunchOpts o;
+  o.op_flags = op_flags;
+  o.done_flag = done_flag;
+  o.seq = seq;
+  return swap_impl(h, dir, ops, n_ops, stream, o);
 }
 
 int kvs_wait_flag(uint64_t stream, const uint32_t* flag, uint32_t value) {

@@ -191,6 +191,19 @@ class SwapDataPlane:
         _lib.check(rc, f"kvs_swap_layered({direction})")
         return arr
 
+    def swap_ops(self, direction: str, ops: OpsLike, op_flags: int, seq: int,
+                 stream: Optional[torch.cuda.Stream] = None,
+                 done_flag: Optional[int] = None) -> np.ndarray:
+        """One launch; op_flags[i] <- seq once TransferOp i has landed."""
+        arr = ops_array(ops)
+        rc = self.lib.kvs_swap_ops(self.handle, _lib.DIRECTIONS[direction],
+                                   arr.ctypes.data_as(ctypes.c_void_p), arr.shape[0],
+                                   _stream_handle(stream), ctypes.c_void_p(op_flags),
+                                   ctypes.c_void_p(done_flag) if done_flag else None,
+                                   seq & 0xFFFFFFFF)
+        _lib.check(rc, f"kvs_swap_ops({direction})")
+        return arr
+
     def baseline(self, direction: str, mode: int, ops: OpsLike,
                  stream: Optional[torch.cuda.Stream] = None) -> None:
         arr = ops_array(ops)

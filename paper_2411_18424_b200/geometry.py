@@ -19,7 +19,73 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .core import BlockSpec
+# ----------------------------------------------------------------------------
+# Scalars the whole swap path shares (mirror of kvswitch/core.py:11-65):
+# simulated time is an int count of microseconds, so replay-mode decisions are
+# bit-exact with the reference; real transfers are timed by CUDA events.
+# kvswitch.core's import path is kept by core.py, which re-exports these.
+# ----------------------------------------------------------------------------
+
+SimTime = int
+RequestId = int
+TurnId = int
+GroupId = int
+
+US_PER_S = 1_000_000
+
+
+def elapsed(later: SimTime, earlier: SimTime) -> SimTime:
+    """Non-negative difference: a clock never runs backwards (core.py:22-24)."""
+    return max(later - earlier, 0)
+
+
+def _at_least_one(owner: object, *names: str) -> None:
+    for n in names:
+        v = getattr(owner, n)
+        if v < 1:
+            raise ValueError(f"{n} must be >= 1, got {v}")
+
+
+@dataclass(frozen=True)
+class BlockSpec:
+    """Tokens per KV block, and the bytes a block moves in one swap."""
+
+    block_size_tokens: int = 16
+    bytes_per_block: int = 131072  # the reference default; KVGeometry.block_spec() sets it per model
+
+    def __post_init__(self) -> None:
+        _at_least_one(self, "block_size_tokens", "bytes_per_block")
+
+
+def blocks_needed(tokens: int, spec: BlockSpec) -> int:
+    """Blocks that hold `tokens` tokens: ceil(tokens / block_size_tokens)."""
+    if tokens < 0:
+        raise ValueError(f"tokens must be >= 0, got {tokens}")
+    return (tokens + spec.block_size_tokens - 1) // spec.block_size_tokens
+
+
+def group_bytes(num_blocks: int, spec: BlockSpec) -> int:
+    """Bytes a run of `num_blocks` consecutive blocks moves."""
+    if num_blocks < 0:
+        raise ValueError(f"num_blocks must be >= 0, got {num_blocks}")
+    return spec.bytes_per_block * num_blocks
+
+
+@dataclass(frozen=True, order=True)
+class Priority:
+    """Scheduling order: lower rank first, then lower request id."""
+
+    rank: int
+    request_id: RequestId
+
+
+def priority_key(rank: int, request_id: RequestId) -> tuple[int, RequestId]:
+    return rank, request_id
+
+
+# ----------------------------------------------------------------------------
+# Model KV shapes per tensor-parallel rank
+# ----------------------------------------------------------------------------
 
 
 @dataclass(frozen=True)

@@ -147,16 +147,30 @@ def _overlaps(a: list[tuple[int, int]], b: list[tuple[int, int]]) -> bool:
     return False
 
 
+def _hit_ops(extents: list[tuple[int, int]], per_op: list[tuple[int, int]]) -> list[int]:
+    """Indices of ops whose extent intersects any of `extents` (half-open)."""
+    hits = []
+    for i, (s1, n1) in enumerate(per_op):
+        e1 = s1 + n1
+        for s0, n0 in extents:
+            if s0 < e1 and s1 < s0 + n0:
+                hits.append(i)
+                break
+    return hits
+
+
 @dataclass
 class TransferRecord:
     direction: str
-    gpu: list[tuple[int, int]]
-    host: list[tuple[int, int]]
+    gpu: list[tuple[int, int]]  # per TransferOp
+    host: list[tuple[int, int]]  # per TransferOp
     event: object  # torch.cuda.Event
     nbytes: int
     refresh_bytes: int
     start_event: object = None
     done: bool = False
+    flag_base: Optional[int] = None  # op-flag slots [flag_base, flag_base + n_ops)
+    seq: int = 0
 
     def poll(self) -> bool:
         if not self.done and self.event.query():
@@ -174,12 +188,24 @@ COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 #   throughput — balanced, highest combined GB/s (bulk migration).
 DUPLEX_POLICIES = {"latency": {"out": 8, "in": 32}, "throughput": {"out": 32, "in": 32}}
 
+# Waiting on more op flags than this costs more driver calls than the
+# plan-level event saves.
+MAX_OP_WAITS = 8
+FLAG_RING = 1 << 20
+
 
 class StreamExecutor:
-    """Real streams + event hazards around one SwapDataPlane (one rank)."""
+    """Real streams + event hazards around one SwapDataPlane (one rank).
+
+    With the kernel path every plan is issued through kvs_swap_ops, so each
+    TransferOp publishes its own completion word: conflicting work waits for
+    the blocking ops only (the reference resolves conflicts per op,
+    swap.py:236-252), falling back to the plan's event when many ops block.
+    """
 
     def __init__(self, dataplane, compute_stream=None, copy_impl: str = "kernel",
-                 timing: bool = False, duplex_policy: str = "latency") -> None:
+                 timing: bool = False, duplex_policy: str = "latency",
+                 op_granular: bool = True) -> None:
         import torch
 
         if copy_impl not in COPY_IMPLS:
@@ -195,12 +221,19 @@ class StreamExecutor:
             torch.cuda.Stream(device=dev, priority=-1)
         self.copy_impl = copy_impl
         self.timing = timing
+        self.op_granular = op_granular and copy_impl == "kernel"
         self.pending: list[TransferRecord] = []
         self.history: list[TransferRecord] = []
         self.bytes = {"out": 0, "in": 0}
         self.refresh_bytes = 0
         self.launches = 0
+        self.op_waits = 0
+        self.plan_waits = 0
         self.block_bytes = dataplane.geometry.block_bytes
+        self._flags = torch.zeros(FLAG_RING, dtype=torch.int32, device=dev)
+        self._flags_ptr = self._flags.data_ptr()
+        self._flag_head = 0
+        self._seq = 0
         self.set_duplex_policy(duplex_policy)
 
     def set_duplex_policy(self, policy: str) -> None:
@@ -212,6 +245,26 @@ class StreamExecutor:
 
     def _prune(self) -> None:
         self.pending = [r for r in self.pending if not r.poll()]
+
+    def _claim_flags(self, n: int) -> int:
+        if self._flag_head + n > FLAG_RING:
+            self._flag_head = 0
+        base = self._flag_head
+        for r in self.pending:  # never recycle slots a live transfer still signals
+            if r.flag_base is not None and r.flag_base < base + n and base < r.flag_base + len(r.gpu):
+                r.event.synchronize()
+        self._flag_head += n
+        return base
+
+    def _wait(self, stream, rec: TransferRecord, ops: list[int]) -> None:
+        """`stream` waits for ops `ops` of `rec` (or the whole plan)."""
+        if rec.flag_base is not None and len(ops) <= MAX_OP_WAITS:
+            for i in ops:
+                self.dp.wait_flag(stream, self._flags_ptr + 4 * (rec.flag_base + i), rec.seq)
+            self.op_waits += len(ops)
+        else:
+            stream.wait_event(rec.event)
+            self.plan_waits += 1
 
     def submit(self, direction: str, ops, split_single: bool = False,
                refresh_blocks: int = 0) -> TransferRecord:
@@ -225,19 +278,33 @@ class StreamExecutor:
         for r in self.pending:
             if r.direction == direction:
                 continue  # same stream: already ordered
+            # out: writes host (WAR/WAW vs r), reads GPU r writes (RAW, r = in);
+            # in:  reads host r = out writes (RAW), writes GPU r touches (WAR/WAW).
             if direction == "out":
-                hazard = _overlaps(host, r.host) or (r.direction == "in" and _overlaps(gpu, r.gpu))
+                hits = set(_hit_ops(host, r.host))
+                if r.direction == "in":
+                    hits |= set(_hit_ops(gpu, r.gpu))
             else:
-                hazard = (r.direction == "out" and _overlaps(host, r.host)) or _overlaps(gpu, r.gpu)
-            if hazard:
-                stream.wait_event(r.event)
+                hits = set(_hit_ops(gpu, r.gpu))
+                if r.direction == "out":
+                    hits |= set(_hit_ops(host, r.host))
+            if hits:
+                self._wait(stream, r, sorted(hits))
         start = None
         if self.timing:
             start = torch.cuda.Event(enable_timing=True)
             start.record(stream)
+        flag_base, seq = None, 0
         if ops:
             if self.copy_impl == "kernel":
-                self.dp.swap(direction, ops, stream=stream)
+                if self.op_granular:
+                    flag_base = self._claim_flags(len(ops))
+                    self._seq += 1
+                    seq = self._seq
+                    self.dp.swap_ops(direction, ops, self._flags_ptr + 4 * flag_base, seq,
+                                     stream=stream)
+                else:
+                    self.dp.swap(direction, ops, stream=stream)
                 self.launches += 1
             else:
                 mode = COPY_IMPLS.index(self.copy_impl) - 1
@@ -246,7 +313,7 @@ class StreamExecutor:
         ev.record(stream)
         blocks = sum(op.blocks for op in ops)
         rec = TransferRecord(direction, gpu, host, ev, blocks * self.block_bytes,
-                             refresh_blocks * self.block_bytes, start)
+                             refresh_blocks * self.block_bytes, start, False, flag_base, seq)
         self.bytes[direction] += rec.nbytes
         self.refresh_bytes += rec.refresh_bytes
         self.pending.append(rec)
@@ -255,14 +322,16 @@ class StreamExecutor:
         return rec
 
     def compute_barrier(self, extents: list[tuple[int, int]]) -> int:
-        """Make the compute stream wait for transfers touching `extents`.
+        """Make the compute stream wait for transfers touching `extents`
+        (their blocking ops only, when op flags exist).
 
         Returns the number of transfers waited on (real conflicts)."""
         self._prune()
         n = 0
         for r in self.pending:
-            if _overlaps(extents, r.gpu):
-                self.compute.wait_event(r.event)
+            hits = _hit_ops(extents, r.gpu)
+            if hits:
+                self._wait(self.compute, r, hits)
                 n += 1
         return n
 

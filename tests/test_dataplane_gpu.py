@@ -276,3 +276,63 @@ def test_layered_swap_flags_each_plane(cuda_ok, direction):
     torch.cuda.synchronize()
     assert flags.tolist() == [2] * geo.num_planes
     host.close()
+
+
+def test_op_flags_signal_each_transfer_op(cuda_ok):
+    """kvs_swap_ops: op i's flag <- seq once op i landed; a consumer waiting
+    on one op's flag sees that op's bytes complete (op-granular conflicts)."""
+    torch = cuda_ok
+    geo = _small_geometry(1028, 4)
+    G = C = 4096
+    cache, host, dp = _mk(torch, geo, G, C, ctas={"out": 2})
+    pattern = orc.kv_pattern(13, geo.num_planes, G, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    host.array[:] = 0
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    ops = orc.random_runs(rng, 1600, 100, G, C)  # 16 ops of 100 blocks
+    flags = torch.zeros(len(ops) + 3000, dtype=torch.int32, device="cuda:0")
+    done = torch.zeros(1, dtype=torch.int32, device="cuda:0")
+    s_swap, s_use = torch.cuda.Stream(), torch.cuda.Stream()
+    dp.swap_ops("out", ops, flags.data_ptr(), 7, stream=s_swap, done_flag=done.data_ptr())
+    k = 3
+    dp.wait_flag(s_use, flags.data_ptr() + 4 * k, 7)
+    b, g, c = (int(x) for x in ops[k])
+    with torch.cuda.stream(s_use):
+        cache.planes[:, g:g + b].fill_(0xEE)  # reuse op k's source blocks early
+    torch.cuda.synchronize()
+    assert flags[:len(ops)].tolist() == [7] * len(ops) and int(done.item()) == 7
+    want = np.zeros((C, geo.block_bytes), np.uint8)
+    orc.apply_plan("out", pattern, want, ops)
+    np.testing.assert_array_equal(host.array, want)  # op k was read before the overwrite
+    # > 2048 ops: flags of every launch slice
+    many = orc.random_runs(rng, 2500, 1, G, C)
+    dp.swap_ops("in", many, flags.data_ptr(), 8, stream=s_swap)
+    torch.cuda.synchronize()
+    assert (flags[:len(many)] == 8).all()
+    host.close()
+
+
+def test_executor_op_granular_conflict_wait(cuda_ok):
+    """StreamExecutor: compute waits on the blocking op's flag, not the plan."""
+    torch = cuda_ok
+    from paper_2411_18424_b200.cpu_store import TransferOp
+    from paper_2411_18424_b200.swap import StreamExecutor
+
+    geo = _small_geometry(1028, 4)
+    cache, host, dp = _mk(torch, geo, 1024, 1024)
+    ex = StreamExecutor(dp)
+    pattern = orc.kv_pattern(17, geo.num_planes, 1024, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    torch.cuda.synchronize()
+    ops = [TransferOp(64, 64 * i, 64 * i) for i in range(10)]
+    ex.submit("out", ops)
+    assert ex.compute_barrier([(64 * 2 + 5, 3)]) == 1  # overlaps op 2 only
+    assert ex.op_waits == 1 and ex.plan_waits == 0
+    with torch.cuda.stream(ex.compute):
+        cache.planes[:, 133:136].fill_(0x11)
+    ex.synchronize()
+    want = np.zeros((1024, geo.block_bytes), np.uint8)
+    orc.apply_plan("out", pattern, want, [(o.blocks, o.gpu_start, o.cpu_start) for o in ops])
+    np.testing.assert_array_equal(host.array[:640], want[:640])
+    host.close()
