@@ -452,7 +452,7 @@ def run_trace(args, geo, dev):
         out["runs"][name] = {"ablation": mode, "copy_impl": impl,
                              **{k: lat[k] for k in ("ttft_p50_ms", "ttft_p99_ms", "tbt_p99_ms",
                                                     "tbt_p999_ms", "decode_stall_frac",
-                                                    "wall_s")},
+                                                    "swap_induced_decode_stall", "wall_s")},
                              "tokens": rep.total_tokens,
                              "swap_gib": {"out": round(st["bytes_out"] / 2**30, 2),
                                           "in": round(st["bytes_in"] / 2**30, 2)},

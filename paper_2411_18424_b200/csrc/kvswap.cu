@@ -86,6 +86,37 @@ __device__ __forceinline__ void st_plain(void* p, const int4& v) {
                : "memory");
 }
 
+__device__ __forceinline__ void publish(uint32_t* flag, uint32_t seq) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
+}
+
+// Add a warp's `n` finished pieces of `plane` to the plane's counter; the
+// warp that completes the plane publishes seq.  Warp-uniform call.
+template <int CAP>
+__device__ __forceinline__ void credit_plane(const SwapParams<CAP>& p, uint32_t lane,
+                                             uint32_t plane, uint32_t n) {
+  if (p.plane_flags == nullptr || n == 0) return;
+  __syncwarp();  // every lane's stores precede lane 0's fence
+  if (lane == 0) {
+    __threadfence_system();
+    const unsigned long long old = atomicAdd(p.plane_ctr + plane, static_cast<unsigned long long>(n));
+    if (old + n == p.plane_base + p.pieces_per_plane) publish(p.plane_flags + plane, p.seq);
+  }
+}
+
+// Same for a TransferOp (`want` = all its pieces across planes).
+template <int CAP>
+__device__ __forceinline__ void credit_op(const SwapParams<CAP>& p, uint32_t lane, int op,
+                                          uint32_t n, uint32_t want) {
+  if (p.op_flags == nullptr || n == 0 || op < 0) return;
+  __syncwarp();
+  if (lane == 0) {
+    __threadfence_system();
+    if (atomicAdd(p.op_ctr + op, n) + n == want) publish(p.op_flags + op, p.seq);
+  }
+}
+
 // DIR == KVS_DIR_OUT: HBM plane chunk -> host block image.
 // DIR == KVS_DIR_IN : host block image -> HBM plane chunk.
 template <int DIR, int CAP>
@@ -97,6 +128,10 @@ __global__ void __launch_bounds__(kMaxThreads)
 
   int op = 0;
   int32_t op_begin = 0;
+  const bool tracking = p.plane_flags != nullptr || p.op_flags != nullptr;
+  uint32_t acc_plane = 0xFFFFFFFFu, acc_plane_n = 0;  // uncredited pieces of acc_plane
+  int acc_op = -1;
+  uint32_t acc_op_n = 0, acc_op_want = 0;  // uncredited pieces of acc_op, its total
   for (uint32_t i = warp; i < p.total_pieces; i += nwarps) {
     uint32_t k, plane, piece;
     if (p.layered) {
@@ -146,34 +181,29 @@ __global__ void __launch_bounds__(kMaxThreads)
       for (int j = 0; j < kUnroll; ++j)
         if (j * kWarpBytes + lo < remain) st_plain(dst + j * kWarpBytes + lo, v[j]);
     }
-    if (p.plane_flags != nullptr || p.op_flags != nullptr) {
-      // Fine-grained completion: the warp that retires the last piece of a
-      // plane (layered) or of a TransferOp publishes seq (release, system
-      // scope); every warp fences its stores ahead of its counter increment.
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence_system();
-        if (p.plane_flags != nullptr) {
-          const unsigned long long old = atomicAdd(p.plane_ctr + plane, 1ull);
-          if (old + 1 == p.plane_base + p.pieces_per_plane) {
-            __threadfence_system();
-            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.plane_flags + plane),
-                         "r"(p.seq)
-                         : "memory");
-          }
-        }
-        if (p.op_flags != nullptr) {
-          const uint32_t want = static_cast<uint32_t>(p.op_end[op] - op_begin) * p.num_planes *
-                                p.pieces_per_chunk;
-          if (atomicAdd(p.op_ctr + op, 1u) + 1 == want) {
-            __threadfence_system();
-            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.op_flags + op),
-                         "r"(p.seq)
-                         : "memory");
-          }
-        }
+    if (tracking) {
+      // Credit finished pieces lazily: only when this warp moves to another
+      // plane / op (or exits) does it fence and add its count, so the system
+      // fences scale with (warps x planes), not with pieces.
+      if (p.plane_flags != nullptr && plane != acc_plane) {
+        credit_plane(p, lane, acc_plane, acc_plane_n);
+        acc_plane = plane;
+        acc_plane_n = 0;
       }
+      if (p.op_flags != nullptr && op != acc_op) {
+        credit_op(p, lane, acc_op, acc_op_n, acc_op_want);
+        acc_op = op;
+        acc_op_n = 0;
+        acc_op_want = static_cast<uint32_t>(p.op_end[op] - op_begin) * p.num_planes *
+                      p.pieces_per_chunk;
+      }
+      ++acc_plane_n;
+      ++acc_op_n;
     }
+  }
+  if (tracking) {
+    credit_plane(p, lane, acc_plane, acc_plane_n);
+    credit_op(p, lane, acc_op, acc_op_n, acc_op_want);
   }
 
   if (p.done_flag != nullptr) {
@@ -829,18 +859,24 @@ __global__ void __launch_bounds__(512) kvs_stream_read_kernel(const int4* __rest
                                                               int4* sink) {
   const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  // Power-of-two buffers wrap with a mask; others with a (slow) modulo.
+  const bool pow2 = (buf_vecs & (buf_vecs - 1)) == 0;
+  const uint64_t mask = buf_vecs - 1;
   uint32_t acc = 0;
   uint64_t i = tid;
   // 4 independent 16-B loads in flight per thread.
   for (; i + 3 * step < total_vecs; i += 4 * step) {
     int4 v[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] = ld_stream(buf + (i + j * step) % buf_vecs);
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t x = i + j * step;
+      v[j] = ld_stream(buf + (pow2 ? (x & mask) : (x % buf_vecs)));
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc ^= v[j].x ^ v[j].y ^ v[j].z ^ v[j].w;
   }
   for (; i < total_vecs; i += step) {
-    const int4 v = ld_stream(buf + i % buf_vecs);
+    const int4 v = ld_stream(buf + (pow2 ? (i & mask) : (i % buf_vecs)));
     acc ^= v.x ^ v.y ^ v.z ^ v.w;
   }
   if (acc == 0x9E3779B9u) sink->x = static_cast<int>(acc);  // practically never

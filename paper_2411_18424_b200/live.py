@@ -89,6 +89,11 @@ class DecodeEmulator:
 class LiveStats:
     decode_ms: float = 0.0  # measured decode-kernel time (with concurrent swaps)
     decode_nominal_ms: float = 0.0  # the same bytes at the calibrated solo rate
+    # split by whether swap transfers were in flight when the decode launched
+    busy_ms: float = 0.0
+    busy_nominal_ms: float = 0.0
+    quiet_ms: float = 0.0
+    quiet_nominal_ms: float = 0.0
     iterations: int = 0
     idle_waits: int = 0
     wall_s: float = 0.0
@@ -98,6 +103,14 @@ class LiveStats:
         if self.decode_nominal_ms <= 0:
             return 0.0
         return self.decode_ms / self.decode_nominal_ms - 1.0
+
+    @property
+    def swap_induced_stall(self) -> Optional[float]:
+        """Decode slowdown while swaps run, relative to decode with none in
+        flight in the same run (same clocks, same power state)."""
+        if self.busy_nominal_ms <= 0 or self.quiet_nominal_ms <= 0 or self.quiet_ms <= 0:
+            return None
+        return (self.busy_ms / self.busy_nominal_ms) / (self.quiet_ms / self.quiet_nominal_ms) - 1
 
 
 class LiveEngine(Engine):
@@ -234,6 +247,7 @@ class LiveEngine(Engine):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(compute)
+            swapping = any(not r.poll() for r in ex.pending)
             nbytes = self.decode.launch_us(compute, nominal_us)
             e1.record(compute)
             compute.synchronize()
@@ -243,8 +257,15 @@ class LiveEngine(Engine):
                                 kernel_ms, decision.mode == "sync" and bool(pending),
                                 conf_now, len(prefillers),
                                 len(decoders)))
+            nominal_ms = nbytes / self.decode.bytes_per_us / 1e3
             self.live.decode_ms += kernel_ms
-            self.live.decode_nominal_ms += nbytes / self.decode.bytes_per_us / 1e3
+            self.live.decode_nominal_ms += nominal_ms
+            if swapping:
+                self.live.busy_ms += kernel_ms
+                self.live.busy_nominal_ms += nominal_ms
+            else:
+                self.live.quiet_ms += kernel_ms
+                self.live.quiet_nominal_ms += nominal_ms
             self.live.iterations += 1
             duration = end - start
             emitted = self._emit_tokens(prefillers, decoders, end)
@@ -309,6 +330,10 @@ class LiveEngine(Engine):
             "tbt_p99_ms": pct(self.tbt_samples, 0.99),
             "tbt_p999_ms": pct(self.tbt_samples, 0.999),
             "decode_stall_frac": round(self.live.decode_stall, 4),
+            "swap_induced_decode_stall": (None if self.live.swap_induced_stall is None
+                                          else round(self.live.swap_induced_stall, 4)),
+            "decode_time_with_swaps_frac": round(
+                self.live.busy_ms / max(1e-9, self.live.decode_ms), 4),
             "iterations": self.live.iterations,
             "idle_waits": self.live.idle_waits,
             "wall_s": round(self.live.wall_s, 2),

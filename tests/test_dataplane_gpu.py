@@ -336,3 +336,24 @@ def test_executor_op_granular_conflict_wait(cuda_ok):
     orc.apply_plan("out", pattern, want, [(o.blocks, o.gpu_start, o.cpu_start) for o in ops])
     np.testing.assert_array_equal(host.array[:640], want[:640])
     host.close()
+
+
+def test_registered_numa_host_pool(cuda_ok):
+    """kvs_host_alloc(KVS_HOST_REGISTER): mmap + mbind(node 0) + cudaHostRegister."""
+    torch = cuda_ok
+    from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
+
+    geo = _small_geometry(1024, 2)
+    cache = PagedKVCache(geo, 64, device="cuda:0")
+    host = HostKVPool(64, geo.block_bytes, numa_node=0, register=True)
+    dp = SwapDataPlane(cache, host)
+    pattern = orc.kv_pattern(2, geo.num_planes, 64, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    ops = [(10, 5, 40), (3, 50, 0)]
+    dp.swap("out", ops)
+    torch.cuda.synchronize()
+    want = np.zeros((64, geo.block_bytes), np.uint8)
+    orc.apply_plan("out", pattern, want, ops)
+    np.testing.assert_array_equal(host.array[[*range(40, 50), 0, 1, 2]],
+                                  want[[*range(40, 50), 0, 1, 2]])
+    host.close()
