@@ -304,6 +304,9 @@ def run_ours(args, geo):
     if rank == 0 and not args.no_sweep:
         sweep = group_sweep(dp, s)
 
+    # ---- serving configuration: paced swaps under a concurrent decode load ----
+    serving = serving_interference(dp, dev, s) if rank == 0 else None
+
     # ---- live multi-turn preemption trace: P99 TTFT / TBT (metric part 2) ----
     trace = None
     if not args.no_trace:
@@ -351,6 +354,7 @@ def run_ours(args, geo):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "sweep": sweep,
+            "serving": serving,
             "trace": trace,
         }
         print(json.dumps(line), flush=True)
@@ -460,6 +464,76 @@ def run_trace(args, geo, dev):
         rt.close()
     del decode
     torch_empty_cache()
+    return out
+
+
+def serving_interference(dp, dev, s):
+    """Swap-induced decode stall, measured: 2 ms HBM-streaming decode steps on a
+    high-priority stream while a 2 GiB swap runs, per direction, with the
+    serving ("latency") policy: paced kernels + shared budget (swap.py)."""
+    import statistics
+
+    import torch
+
+    from oracle.bytes_oracle import random_runs
+    from paper_2411_18424_b200.live import DecodeEmulator
+    from paper_2411_18424_b200.swap import DUPLEX_POLICIES
+
+    dec = DecodeEmulator(dev, weight_bytes=16 << 30)
+    comp = torch.cuda.Stream(device=dev, priority=-1)
+    s2 = torch.cuda.Stream(device=dev)
+    rng = np.random.default_rng(5)
+    n = 1024
+    ops = random_runs(rng, n, 16, POOL_BLOCKS // 2, POOL_BLOCKS // 2).astype(np.int32)
+    ops_in = ops.copy()
+    ops_in[:, 1:] += POOL_BLOCKS // 2
+    nbytes = n * dp.geometry.block_bytes
+
+    def steps(k):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
+        evs[0].record(comp)
+        for i in range(k):
+            dec.launch_us(comp, 2000.0)
+            evs[i + 1].record(comp)
+        return evs
+
+    steps(3)
+    torch.cuda.synchronize()
+    ev = steps(20)
+    torch.cuda.synchronize()
+    solo = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(20))
+    pol = DUPLEX_POLICIES["latency"]
+    for d in ("out", "in"):
+        c, t, pace = pol[d]
+        dp.set_launch(d, c, t)
+        dp.set_pace(d, pace)
+    dp.set_budget(pol["budget"])
+    out = {"policy": "latency", "decode_step_solo_ms": round(solo, 3), "runs": {}}
+    for name, dirs in (("out", ("out",)), ("in", ("in",)), ("duplex", ("out", "in"))):
+        torch.cuda.synchronize()
+        t = {}
+        for d in dirs:
+            st = s if d == "out" else s2
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            dp.swap(d, ops if d == "out" else ops_in, stream=st)
+            e1.record(st)
+            t[d] = (e0, e1)
+        ev = steps(40)
+        torch.cuda.synchronize()
+        end = max(t[d][0].elapsed_time(t[d][1]) for d in dirs)
+        st_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(40)
+                 if t[dirs[0]][0].elapsed_time(ev[i]) <= end]
+        out["runs"][name] = {
+            "swap_gbs": {d: round(nbytes / (t[d][0].elapsed_time(t[d][1]) * 1e-3) / 1e9, 2)
+                         for d in dirs},
+            "decode_steps": len(st_ms),
+            "decode_slowdown": round(statistics.median(st_ms) / solo - 1, 4) if st_ms else None}
+    for d in ("out", "in"):
+        dp.set_launch(d, 0, 0)
+        dp.set_pace(d, 0.0)
+    dp.set_budget(0.0)
+    del dec
     return out
 
 

@@ -102,6 +102,19 @@ int kvs_set_launch(KvsHandle* h, int dir, int ctas, int threads);
  * bulk path's smem ring (0 = defaults: 16 KiB x 4); ignored by the LSU path. */
 int kvs_set_path(KvsHandle* h, int dir, int path, int piece_bytes, int stages);
 
+/* Pace one direction's LSU kernel to `gbps` GB/s (0 = unpaced).  Stores to
+ * host memory issued faster than PCIe drains them queue up in the XBAR/L2
+ * path the decode kernels' HBM traffic shares; holding the grid to the link
+ * rate keeps swap-induced decode stall bounded (north star <= 10%).
+ * Replaces the reference's bounded dispatch yield (swap.py:256-268). */
+int kvs_set_pace(KvsHandle* h, int dir, double gbps);
+
+/* One rate budget shared by both directions of this handle (0 = none): a
+ * token bucket on the GPU global timer, drawn per piece by swap-out and
+ * swap-in kernels alike, so a concurrent preempt + resume cannot add up to
+ * more host-link traffic than decode tolerates. */
+int kvs_set_budget(KvsHandle* h, double gbps);
+
 /* Queue one SwapPlan's bytes on `stream` — asynchronous, no host blocking,
  * no allocation.  Replaces the modeled copy-engine timeline of
  * SwapManager.dispatch (swap.py:193-205, costmodel.py:29-31).

@@ -67,6 +67,10 @@ struct SwapParams {
   uint32_t* plane_flags;       // [num_planes]: receives seq when a plane has landed
   uint32_t* op_ctr;            // [n_ops] piece counters, zeroed before the launch
   uint32_t* op_flags;          // [n_ops]: receives seq when a TransferOp has landed
+  uint64_t pace_ps;            // >0: piece i may start no earlier than t0 + i*pace_ps
+  unsigned long long* bucket;  // shared (both directions) budget clock, ns
+  uint64_t bucket_cost_ns;     // >0: ns of budget one piece consumes
+  uint64_t bucket_burst_ns;    // idle credit cap
   int32_t op_end[CAP];         // inclusive prefix sum of TransferOp.blocks
   int32_t op_gpu[CAP];         // TransferOp.gpu_start
   int32_t op_cpu[CAP];         // TransferOp.cpu_start
@@ -84,6 +88,20 @@ __device__ __forceinline__ void st_plain(void* p, const int4& v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
                "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Reserve `cost` ns on the shared budget clock; returns the reserved start.
+__device__ __forceinline__ unsigned long long take_budget(unsigned long long* bucket,
+                                                          uint64_t cost, uint64_t burst) {
+  const unsigned long long now = globaltimer_ns();
+  atomicMax(bucket, now > burst ? now - burst : 0ull);  // idle credit is capped
+  return atomicAdd(bucket, static_cast<unsigned long long>(cost));
 }
 
 __device__ __forceinline__ void publish(uint32_t* flag, uint32_t seq) {
@@ -128,6 +146,7 @@ __global__ void __launch_bounds__(kMaxThreads)
 
   int op = 0;
   int32_t op_begin = 0;
+  const uint64_t t0 = p.pace_ps != 0 ? globaltimer_ns() : 0;
   const bool tracking = p.plane_flags != nullptr || p.op_flags != nullptr;
   uint32_t acc_plane = 0xFFFFFFFFu, acc_plane_n = 0;  // uncredited pieces of acc_plane
   int acc_op = -1;
@@ -155,6 +174,21 @@ __global__ void __launch_bounds__(kMaxThreads)
     while (static_cast<int32_t>(k) >= p.op_end[op]) {
       op_begin = p.op_end[op];
       ++op;
+    }
+    if (p.pace_ps != 0) {
+      // Rate pacing: posted sysmem stores (and, less so, non-posted reads)
+      // issued faster than PCIe drains them back up the XBAR/L2 queues the
+      // decode kernel's HBM traffic shares.  Hold the grid to the link rate.
+      const uint64_t due = t0 + (static_cast<uint64_t>(i) * p.pace_ps) / 1000u;
+      while (globaltimer_ns() < due) __nanosleep(64);
+    }
+    if (p.bucket_cost_ns != 0) {
+      // Shared budget: swap-out and swap-in of this handle together stay
+      // under one rate, whatever their mix (a token bucket on a global clock).
+      unsigned long long slot = 0;
+      if (lane == 0) slot = take_budget(p.bucket, p.bucket_cost_ns, p.bucket_burst_ns);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      while (globaltimer_ns() < slot) __nanosleep(64);
     }
     const int64_t rel = static_cast<int64_t>(k) - op_begin;
     const int64_t off = static_cast<int64_t>(piece) * kPieceBytes;
@@ -324,10 +358,24 @@ __global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant
     int lop = 0, sop = 0;          // op cursors: loads run ahead of stores
     int32_t lbeg = 0, sbeg = 0;
     uint32_t phase_bits = 0;
+    const uint64_t t0 = p.pace_ps != 0 ? globaltimer_ns() : 0;
+    // Pacing (kvs_set_pace): piece i's load may not issue before t0 + i*pace.
+    auto pace = [&](uint32_t i) {
+      if (p.pace_ps != 0) {
+        const uint64_t due = t0 + (static_cast<uint64_t>(i) * p.pace_ps) / 1000u;
+        while (globaltimer_ns() < due) __nanosleep(64);
+      }
+      if (p.bucket_cost_ns != 0) {
+        const unsigned long long slot = take_budget(p.bucket, p.bucket_cost_ns,
+                                                    p.bucket_burst_ns);
+        while (globaltimer_ns() < slot) __nanosleep(64);
+      }
+    };
     const uint32_t pre = n < S - 1 ? n : S - 1;
     for (uint32_t j = 0; j < pre; ++j) {
       const char* src;
       char* dst;
+      pace(first + j * gridDim.x);
       const uint32_t b = bulk_piece<DIR>(p, first + j * gridDim.x, lop, lbeg, src, dst);
       mbar_expect_tx(&bars[j % S], b);
       bulk_load(ring + (j % S) * p.piece_bytes, src, b, &bars[j % S]);
@@ -347,6 +395,7 @@ __global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant
         bulk_wait_read<1>();
         const char* s2;
         char* d2;
+        pace(first + jj * gridDim.x);
         const uint32_t b2 = bulk_piece<DIR>(p, first + jj * gridDim.x, lop, lbeg, s2, d2);
         mbar_expect_tx(&bars[jj % S], b2);
         bulk_load(ring + (jj % S) * p.piece_bytes, s2, b2, &bars[jj % S]);
@@ -388,6 +437,9 @@ struct KvsHandle {
   unsigned long long plane_next[2] = {0, 0};
   int piece_bytes[2] = {0, 0};
   int stages[2] = {0, 0};
+  uint64_t pace_ps[2] = {0, 0};  // per 4 KiB piece; 0 = unpaced
+  double budget_gbps = 0.0;      // shared by both directions; 0 = none
+  unsigned long long* d_bucket = nullptr;
   int64_t launches = 0;
 };
 
@@ -470,6 +522,13 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   if (o.plane_flags != nullptr) h->plane_next[dir] += p.pieces_per_plane;
   p.op_ctr = h->d_op_ctr + static_cast<size_t>(dir) * kOpsPerLaunchMax;
   p.op_flags = o.op_flags;
+  // pace_ps is per 4 KiB; the bulk path paces per (larger) TMA piece.
+  p.pace_ps = h->pace_ps[dir] * static_cast<uint64_t>(piece) / kPieceBytes;
+  p.bucket = h->d_bucket;
+  p.bucket_cost_ns =
+      h->budget_gbps > 0.0 ? static_cast<uint64_t>(piece / h->budget_gbps + 0.5) : 0;
+  if (p.bucket_cost_ns == 0 && h->budget_gbps > 0.0) p.bucket_cost_ns = 1;
+  p.bucket_burst_ns = 16 * p.bucket_cost_ns;
   if (o.op_flags != nullptr) {
     // Same stream as the kernel: ordered before it, and after the previous
     // launch of this direction that used the counters.
@@ -589,6 +648,8 @@ int kvs_create(int device, const KvsGeometry* geo, const uint64_t* plane_ptrs, v
     rc = cuda_rc(
         cudaMemset(h->d_plane_ctr, 0, 2 * sizeof(unsigned long long) * geo->num_planes));
   if (!rc) rc = cuda_rc(cudaMalloc(&h->d_op_ctr, 2 * sizeof(uint32_t) * kOpsPerLaunchMax));
+  if (!rc) rc = cuda_rc(cudaMalloc(&h->d_bucket, sizeof(unsigned long long)));
+  if (!rc) rc = cuda_rc(cudaMemset(h->d_bucket, 0, sizeof(unsigned long long)));
   if (rc) {
     kvs_destroy(h);
     return rc;
@@ -604,6 +665,7 @@ int kvs_destroy(KvsHandle* h) {
   if (h->d_tickets) cudaFree(h->d_tickets);
   if (h->d_plane_ctr) cudaFree(h->d_plane_ctr);
   if (h->d_op_ctr) cudaFree(h->d_op_ctr);
+  if (h->d_bucket) cudaFree(h->d_bucket);
   delete h;
   return KVS_OK;
 }
@@ -613,6 +675,21 @@ int kvs_set_launch(KvsHandle* h, int dir, int ctas, int threads) {
   if (ctas < 0 || threads < 0 || threads % 32 || threads > kMaxThreads) return KVS_ERR_INVALID;
   h->ctas[dir] = ctas;
   h->threads[dir] = threads;
+  return KVS_OK;
+}
+
+int kvs_set_pace(KvsHandle* h, int dir, double gbps) {
+  if (h == nullptr || (dir != KVS_DIR_OUT && dir != KVS_DIR_IN) || !(gbps >= 0.0) ||
+      gbps > 1e6)
+    return KVS_ERR_INVALID;
+  // ps per 4 KiB piece at `gbps` GB/s (1 GB/s = 1 byte/ns).
+  h->pace_ps[dir] = gbps == 0.0 ? 0 : static_cast<uint64_t>(kPieceBytes * 1000.0 / gbps + 0.5);
+  return KVS_OK;
+}
+
+int kvs_set_budget(KvsHandle* h, double gbps) {
+  if (h == nullptr || !(gbps >= 0.0) || gbps > 1e6) return KVS_ERR_INVALID;
+  h->budget_gbps = gbps;
   return KVS_OK;
 }
 

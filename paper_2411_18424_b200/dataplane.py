@@ -164,6 +164,15 @@ class SwapDataPlane:
         _lib.check(self.lib.kvs_set_path(self.handle, _lib.DIRECTIONS[direction],
                                          _lib.PATHS[path], piece_bytes, stages), "kvs_set_path")
 
+    def set_pace(self, direction: str, gbps: float = 0.0) -> None:
+        """Hold one direction's LSU kernel to `gbps` GB/s (0 = unpaced)."""
+        _lib.check(self.lib.kvs_set_pace(self.handle, _lib.DIRECTIONS[direction], float(gbps)),
+                   "kvs_set_pace")
+
+    def set_budget(self, gbps: float = 0.0) -> None:
+        """One GB/s budget shared by swap-out and swap-in (0 = none)."""
+        _lib.check(self.lib.kvs_set_budget(self.handle, float(gbps)), "kvs_set_budget")
+
     @property
     def launches(self) -> int:
         return int(self.lib.kvs_launch_count(self.handle))

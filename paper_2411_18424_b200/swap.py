@@ -180,13 +180,21 @@ class TransferRecord:
 
 COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 
-# Swap-kernel CTAs per direction.  Both directions alone saturate PCIe with
-# >= 4-8 CTAs; they differ when swap-out and swap-in overlap
-# (profiles/r01_duplex_bw.json):
-#   latency    — swap-in keeps ~50 GB/s, swap-out takes what is left (serving:
-#                resumption gates TTFT, swap-out only gates host-space reuse);
-#   throughput — balanced, highest combined GB/s (bulk migration).
-DUPLEX_POLICIES = {"latency": {"out": 8, "in": 32}, "throughput": {"out": 32, "in": 32}}
+# Launch shape and pacing per direction (profiles/r01_interference_*.json,
+# profiles/r01_duplex_bw.json).  Unpaced, SM stores/loads to host memory are
+# issued far faster than PCIe drains them and back up the XBAR/L2 queues that
+# decode's HBM traffic shares: a concurrent 2 ms decode step slowed 1.2-4.9x.
+# Paced to the link rate the same swaps cost decode ~2% (out) / ~9% (in):
+#   latency    — serving: out 8x512 @52 GB/s, in 148x32 @50 GB/s, both
+#                directions together capped at 60 GB/s (shared budget);
+#   throughput — bulk migration: unpaced, balanced 32x512 each way
+#                (highest combined GB/s, decode pays for it);
+#   unpaced    — out 8x512, in 32x512, no pacing (round-1 default shape).
+DUPLEX_POLICIES = {
+    "latency": {"out": (8, 512, 52.0), "in": (148, 32, 50.0), "budget": 60.0},
+    "throughput": {"out": (32, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
+    "unpaced": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
+}
 
 # Waiting on more op flags than this costs more driver calls than the
 # plan-level event saves.
@@ -239,8 +247,12 @@ class StreamExecutor:
     def set_duplex_policy(self, policy: str) -> None:
         if policy not in DUPLEX_POLICIES:
             raise ValueError(f"duplex policy must be one of {sorted(DUPLEX_POLICIES)}")
-        for direction, ctas in DUPLEX_POLICIES[policy].items():
-            self.dp.set_launch(direction, ctas, 0)
+        pol = DUPLEX_POLICIES[policy]
+        for direction in ("out", "in"):
+            ctas, threads, pace = pol[direction]
+            self.dp.set_launch(direction, ctas, threads)
+            self.dp.set_pace(direction, pace)
+        self.dp.set_budget(pol["budget"])
         self.duplex_policy = policy
 
     def _prune(self) -> None:

@@ -357,3 +357,49 @@ def test_registered_numa_host_pool(cuda_ok):
     np.testing.assert_array_equal(host.array[[*range(40, 50), 0, 1, 2]],
                                   want[[*range(40, 50), 0, 1, 2]])
     host.close()
+
+
+@pytest.mark.parametrize("path", ["lsu", "bulk"])
+def test_pacing_and_shared_budget(cuda_ok, path):
+    """kvs_set_pace / kvs_set_budget: the rate is honoured and bytes stay exact."""
+    torch = cuda_ok
+    from paper_2411_18424_b200.geometry import LLAMA3_8B
+
+    G = C = 1024
+    cache, host, dp = _mk(torch, LLAMA3_8B, G, C, path=path)
+    gen = torch.Generator(device="cuda:0").manual_seed(1)
+    cache.planes.view(torch.int32).random_(generator=gen)
+    rng = np.random.default_rng(9)
+    ops = orc.random_runs(rng, 256, 16, G // 2, C // 2)  # 512 MiB
+    ops_in = ops.copy()
+    ops_in[:, 1:] += G // 2
+    nbytes = 256 * LLAMA3_8B.block_bytes
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn, stream):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        return e0, e1
+
+    dp.set_pace("out", 20.0)
+    e = timed(lambda: dp.swap("out", ops, stream=s1), s1)
+    torch.cuda.synchronize()
+    gbs = nbytes / (e[0].elapsed_time(e[1]) * 1e-3) / 1e9
+    assert 17.0 < gbs < 20.6, gbs
+    want = np.zeros((C, LLAMA3_8B.block_bytes), np.uint8)
+    orc.apply_plan("out", cache.planes.cpu().numpy(), want, ops)
+    host_rows = np.concatenate([np.arange(c, c + b) for b, g, c in ops])
+    np.testing.assert_array_equal(host.array[host_rows], want[host_rows])
+    # shared budget: both directions together <= 30 GB/s
+    dp.set_pace("out", 0.0)
+    dp.set_budget(30.0)
+    eo = timed(lambda: dp.swap("out", ops, stream=s1), s1)
+    ei = timed(lambda: dp.swap("in", ops_in, stream=s2), s2)
+    torch.cuda.synchronize()
+    span = max(eo[0].elapsed_time(eo[1]), ei[0].elapsed_time(ei[1]))
+    total = 2 * nbytes / (span * 1e-3) / 1e9
+    assert total < 31.5, total
+    dp.set_budget(0.0)
+    host.close()

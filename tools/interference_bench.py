@@ -63,47 +63,66 @@ def main():
     results = {"decode_step_solo_ms": round(solo, 4), "runs": []}
     print(json.dumps(results), flush=True)
 
+    # (label, path, {dir: (ctas, threads)}, {dir: pace GB/s}, impl, dirs)
+    # impl: kernel | ce_batch | ce_per_run
+    sweep = os.environ.get("SWEEP", "in")
     configs = []
-    for path, ctas, extra in (("lsu", 4, {}), ("lsu", 8, {}), ("lsu", 32, {}),
-                              ("bulk", 8, {"piece": 16384, "stages": 4}),
-                              ("bulk", 16, {"piece": 16384, "stages": 4}),
-                              ("bulk", 64, {"piece": 16384, "stages": 4})):
-        for dirs in (("in",), ("out",), ("out", "in")):
-            configs.append((path, ctas, extra, dirs))
-    for path, ctas, extra, dirs in configs:
+    if sweep == "in":
+        for ct in ((16, 512), (32, 128), (64, 64), (148, 32)):
+            for pace in (0.0, 48.0, 40.0):
+                configs.append((f"lsu{ct[0]}x{ct[1]}", "lsu", {"out": (8, 512), "in": ct},
+                                {"out": 0.0, "in": pace}, "kernel", ("in",)))
+        for ctas in (16, 148):
+            for pace in (0.0, 48.0, 40.0):
+                configs.append((f"bulk{ctas}", "bulk", {"out": (ctas, 32), "in": (ctas, 32)},
+                                {"out": 0.0, "in": pace}, "kernel", ("in",)))
+    else:
+        for pace in (48.0, 52.0):
+            configs.append(("lsu8x512", "lsu", {"out": (8, 512), "in": (148, 32)},
+                            {"out": pace, "in": 0.0}, "kernel", ("out",)))
+        configs.append(("bulk16", "bulk", {"out": (16, 32), "in": (16, 32)},
+                        {"out": 48.0, "in": 0.0}, "kernel", ("out",)))
+        for po, pi in ((20.0, 30.0), (25.0, 25.0), (30.0, 30.0), (15.0, 40.0)):
+            configs.append(("lsu_duplex", "lsu", {"out": (8, 512), "in": (148, 32)},
+                            {"out": po, "in": pi}, "kernel", ("out", "in")))
+    for label, path, ctas, pace, impl, dirs in configs:
         for d in ("out", "in"):
-            dp.set_path(d, path, extra.get("piece", 0), extra.get("stages", 0))
-            dp.set_launch(d, ctas if path == "bulk" else (ctas if d == "in" or len(dirs) == 1
-                                                          else 8), 0)
+            dp.set_path(d, path, 16384 if path == "bulk" else 0, 4 if path == "bulk" else 0)
+            dp.set_launch(d, ctas[d][0], ctas[d][1] if path == "lsu" else 0)
+            dp.set_pace(d, pace[d])
         torch.cuda.synchronize()
         t = {}
         for d in dirs:
             st = s_out if d == "out" else s_in
+            ops = ops_out if d == "out" else ops_in
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            dp.swap(d, ops_out if d == "out" else ops_in, stream=st)
+            if impl == "kernel":
+                dp.swap(d, ops, stream=st)
+            else:
+                dp.baseline(d, 2 if impl == "ce_batch" else 1, ops, stream=st)
             e1.record(st)
             t[d] = (e0, e1)
-        # decode steps while the swaps run (only steps that start before the swaps end count)
-        evs = decode_steps(dec, comp, 60)
+        # decode steps while the swaps run (steps that start before the swaps end count)
+        evs = decode_steps(dec, comp, 80)
         torch.cuda.synchronize()
         swap_end = max(t[d][0].elapsed_time(t[d][1]) for d in dirs)
-        steps, acc = [], 0.0
-        base = evs[0]
-        for i in range(60):
-            start = t[dirs[0]][0].elapsed_time(evs[i])  # step start relative to swap start
-            if start > swap_end:
+        steps = []
+        for i in range(80):
+            if t[dirs[0]][0].elapsed_time(evs[i]) > swap_end:
                 break
             steps.append(evs[i].elapsed_time(evs[i + 1]))
-        row = {"path": path, "ctas": ctas, "dirs": "+".join(dirs),
-               "decode_steps_overlapped": len(steps),
+        row = {"config": label, "impl": impl, "pace_gbs": pace, "ctas": ctas,
+               "dirs": "+".join(dirs), "decode_steps_overlapped": len(steps),
                "decode_slowdown": round(statistics.median(steps) / solo - 1, 4) if steps else None,
+               "decode_slowdown_mean": round(statistics.mean(steps) / solo - 1, 4) if steps else None,
                "swap_gbs": {d: round(nbytes / (t[d][0].elapsed_time(t[d][1]) * 1e-3) / 1e9, 2)
                             for d in dirs}}
         results["runs"].append(row)
         print(json.dumps(row), flush=True)
     for d in ("out", "in"):
         dp.set_path(d, "lsu")
+        dp.set_pace(d, 0.0)
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/interference.json", "w") as f:
         json.dump(results, f, indent=1)
