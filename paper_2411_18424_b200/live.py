@@ -58,6 +58,7 @@ class DecodeEmulator:
         self.weights = torch.empty(weight_bytes, dtype=torch.uint8, device=self.device)
         self.weights.view(torch.int32).random_()
         self.sink = torch.zeros(4, dtype=torch.int32, device=self.device)
+        torch.cuda.synchronize(self.device)  # calibrate on an idle GPU
         self.ctas = ctas
         self.bytes_per_us = self.calibrate()
 
@@ -76,6 +77,7 @@ class DecodeEmulator:
     def calibrate(self, nbytes: int = 8 << 30) -> float:
         s = torch.cuda.Stream(device=self.device)
         self.launch(s, nbytes)
+        s.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
         for _ in range(3):

@@ -37,14 +37,16 @@ class KVIntegrityError(AssertionError):
 class Runtime:
     def __init__(self, geometry: KVGeometry, gpu_blocks: int, cpu_blocks: int,
                  device="cuda:0", copy_impl: str = "kernel", write_kv: bool = True,
-                 verify: bool = False, timing: bool = False) -> None:
+                 verify: bool = False, timing: bool = False,
+                 duplex_policy: str = "latency") -> None:
         if geometry.split_kv:
             raise ValueError("runtime token writes assume fused K/V planes")
         self.geometry = geometry
         self.cache = PagedKVCache(geometry, gpu_blocks, device=device)
         self.host = HostKVPool(cpu_blocks, geometry.block_bytes)
         self.dataplane = SwapDataPlane(self.cache, self.host)
-        self.executor = StreamExecutor(self.dataplane, copy_impl=copy_impl, timing=timing)
+        self.executor = StreamExecutor(self.dataplane, copy_impl=copy_impl, timing=timing,
+                                       duplex_policy=duplex_policy)
         self.write_kv = write_kv
         self.verify = verify
         self.verified = 0

@@ -387,7 +387,7 @@ def test_pacing_and_shared_budget(cuda_ok, path):
     e = timed(lambda: dp.swap("out", ops, stream=s1), s1)
     torch.cuda.synchronize()
     gbs = nbytes / (e[0].elapsed_time(e[1]) * 1e-3) / 1e9
-    assert 17.0 < gbs < 20.6, gbs
+    assert 14.0 < gbs < 21.0, gbs  # paced to 20 GB/s (globaltimer slots)
     want = np.zeros((C, LLAMA3_8B.block_bytes), np.uint8)
     orc.apply_plan("out", cache.planes.cpu().numpy(), want, ops)
     host_rows = np.concatenate([np.arange(c, c + b) for b, g, c in ops])
@@ -400,6 +400,6 @@ def test_pacing_and_shared_budget(cuda_ok, path):
     torch.cuda.synchronize()
     span = max(eo[0].elapsed_time(eo[1]), ei[0].elapsed_time(ei[1]))
     total = 2 * nbytes / (span * 1e-3) / 1e9
-    assert total < 31.5, total
+    assert total < 33.0, total  # shared 30 GB/s budget (+ idle burst credit)
     dp.set_budget(0.0)
     host.close()

@@ -36,7 +36,7 @@ def run_one(args, mode, impl, decode, geo):
     cfg, wl, _ = mconfig.build(doc)
     cfg = type(cfg)(**{**cfg.__dict__, "transfer": b200_transfer_params(args.pcie_gbs)})
     rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, copy_impl=impl,
-                 verify=args.verify, timing=True)
+                 verify=args.verify, timing=True, duplex_policy=args.policy)
     eng = LiveEngine(cfg, generate(wl), rt, decode)
     t0 = time.perf_counter()
     rep = eng.run()
@@ -60,6 +60,12 @@ def run_one(args, mode, impl, decode, geo):
                                                              if r.direction == d)}
                  for d in ("out", "in")},
         "runtime": st,
+        "slowest_transfers_ms": sorted(
+            ((round(r.start_event.elapsed_time(r.event), 2), r.direction, len(r.gpu),
+              r.nbytes >> 20) for r in ex.history if r.start_event is not None),
+            reverse=True)[:8],
+        "slowest_iterations": sorted(eng._trace, reverse=True)[:8],
+        "ttft_top": sorted(eng.ttft_samples, reverse=True)[:8],
     }
     rt.close()
     return out
@@ -79,6 +85,7 @@ def main():
     ap.add_argument("--modes", default="full:kernel,baseline:ce_per_block")
     ap.add_argument("--weights-gib", type=int, default=16)
     ap.add_argument("--verify", action="store_true")
+    ap.add_argument("--policy", default="latency")
     ap.add_argument("--out", default="gpurun_out/live_trace.json")
     args = ap.parse_args()
     geo = PRESETS[args.model]
@@ -88,7 +95,9 @@ def main():
         mode, impl = item.split(":")
         res = run_one(args, mode, impl, decode, geo)
         results["runs"].append(res)
-        print(json.dumps({k: res[k] for k in ("mode", "copy_impl", "wall_s", "latency", "swap")}),
+        print(json.dumps({k: res[k] for k in ("mode", "copy_impl", "wall_s", "latency", "swap",
+                                              "slowest_transfers_ms", "slowest_iterations",
+                                              "ttft_top")}),
               flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
