@@ -211,6 +211,7 @@ class LiveEngine(Engine):
             e_pre = torch.cuda.Event(enable_timing=True)
             e_pre.record(compute)  # GPU-side waits of this iteration start here
             conf_now = ex.compute_barrier(grants) if grants else 0
+            grant_waits = list(ex.last_barrier) if grants else []
             self.conflict_count += conf_now
 
             pending = [f for f in self.manager.in_flight if f.direction == "in"]
@@ -246,6 +247,7 @@ class LiveEngine(Engine):
             nominal_us = iteration_time(prefill_tokens, len(decoders), self.infer) * self.time_scale
             t_cpu = time.perf_counter()
             self.runtime.compute(self, spans)
+            waits_seen = grant_waits + list(ex.last_barrier)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(compute)
@@ -258,7 +260,7 @@ class LiveEngine(Engine):
             self._trace.append((end - start, int((t_cpu - t_iter) * 1e6), e_pre.elapsed_time(e0),
                                 kernel_ms, decision.mode == "sync" and bool(pending),
                                 conf_now, len(prefillers),
-                                len(decoders)))
+                                len(decoders), waits_seen[:6]))
             nominal_ms = nbytes / self.decode.bytes_per_us / 1e3
             self.live.decode_ms += kernel_ms
             self.live.decode_nominal_ms += nominal_ms

@@ -26,6 +26,7 @@ Two layers, one object:
 
 from __future__ import annotations
 
+import time
 from collections import deque
 from dataclasses import dataclass, field
 from typing import Iterable, Optional
@@ -171,6 +172,8 @@ class TransferRecord:
     done: bool = False
     flag_base: Optional[int] = None  # op-flag slots [flag_base, flag_base + n_ops)
     seq: int = 0
+    submitted: float = 0.0  # host perf_counter at submit (diagnostics)
+    deps: int = 0  # cross-stream waits this transfer was issued behind
 
     def poll(self) -> bool:
         if not self.done and self.event.query():
@@ -237,6 +240,7 @@ class StreamExecutor:
         self.launches = 0
         self.op_waits = 0
         self.plan_waits = 0
+        self.last_barrier: list[tuple] = []
         self.block_bytes = dataplane.geometry.block_bytes
         self._flags = torch.zeros(FLAG_RING, dtype=torch.int32, device=dev)
         self._flags_ptr = self._flags.data_ptr()
@@ -287,6 +291,7 @@ class StreamExecutor:
         stream = self.streams[direction]
         if direction == "out":
             stream.wait_stream(self.compute)
+        deps = 0
         for r in self.pending:
             if r.direction == direction:
                 continue  # same stream: already ordered
@@ -302,6 +307,7 @@ class StreamExecutor:
                     hits |= set(_hit_ops(host, r.host))
             if hits:
                 self._wait(stream, r, sorted(hits))
+                deps += 1
         start = None
         if self.timing:
             start = torch.cuda.Event(enable_timing=True)
@@ -325,7 +331,8 @@ class StreamExecutor:
         ev.record(stream)
         blocks = sum(op.blocks for op in ops)
         rec = TransferRecord(direction, gpu, host, ev, blocks * self.block_bytes,
-                             refresh_blocks * self.block_bytes, start, False, flag_base, seq)
+                             refresh_blocks * self.block_bytes, start, False, flag_base, seq,
+                             time.perf_counter(), deps)
         self.bytes[direction] += rec.nbytes
         self.refresh_bytes += rec.refresh_bytes
         self.pending.append(rec)
@@ -340,10 +347,14 @@ class StreamExecutor:
         Returns the number of transfers waited on (real conflicts)."""
         self._prune()
         n = 0
+        self.last_barrier = []  # (direction, age_ms, ops waited, its deps, MiB)
         for r in self.pending:
             hits = _hit_ops(extents, r.gpu)
             if hits:
                 self._wait(self.compute, r, hits)
+                self.last_barrier.append((r.direction, round((time.perf_counter() - r.submitted)
+                                                             * 1e3, 2), len(hits), r.deps,
+                                          r.nbytes >> 20))
                 n += 1
         return n
 
