@@ -42,6 +42,7 @@ METRIC = "KV swap GB/s vs PCIe peak per GPU; P99 TTFT/TBT on multi-turn preempti
 PCIE_GEN5_X16_GBS = 63.0  # 64 GT/s raw per direction after 128b/130b
 PLAN_BLOCKS = 4096
 POOL_BLOCKS = 8192
+HOST_POOL_BLOCKS = 5120  # 10 GiB pinned per rank (x8 ranks on one host)
 
 
 def parse():
@@ -55,7 +56,7 @@ def parse():
     ap.add_argument("--ctas", type=int, default=0)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--trace-convs", type=int, default=24)
+    ap.add_argument("--trace-convs", type=int, default=64)
     ap.add_argument("--no-trace", action="store_true")
     return ap.parse_args()
 
@@ -140,8 +141,8 @@ class ClockSampler:
 def make_plans(group: int, seed: int):
     from oracle.bytes_oracle import random_runs  # seeded plan generator (test infra)
     rng = np.random.default_rng(seed)
-    out_ops = random_runs(rng, PLAN_BLOCKS, group, POOL_BLOCKS, POOL_BLOCKS)
-    in_ops = random_runs(rng, PLAN_BLOCKS, group, POOL_BLOCKS, POOL_BLOCKS)
+    out_ops = random_runs(rng, PLAN_BLOCKS, group, POOL_BLOCKS, HOST_POOL_BLOCKS)
+    in_ops = random_runs(rng, PLAN_BLOCKS, group, POOL_BLOCKS, HOST_POOL_BLOCKS)
     # swap-in reads back exactly the host blocks swap-out wrote
     host_blocks = np.concatenate([np.arange(c, c + b) for b, g, c in out_ops])
     gpu_blocks = np.concatenate([np.arange(g, g + b) for b, g, c in in_ops])
@@ -240,7 +241,7 @@ def run_ours(args, geo):
         dist.init_process_group("nccl", device_id=dev)
 
     cache = PagedKVCache(geo, POOL_BLOCKS, device=dev)
-    host = HostKVPool(POOL_BLOCKS, geo.block_bytes)
+    host = HostKVPool(HOST_POOL_BLOCKS, geo.block_bytes)
     dp = SwapDataPlane(cache, host, ctas={"out": args.ctas, "in": args.ctas})
     cache.planes.view(torch.int32).random_()
     out_ops, in_ops = make_plans(args.group, seed=rank)
@@ -374,10 +375,10 @@ def run_e2e(args, geo, dp, dev, barrier, world):
 
     ex = StreamExecutor(dp, duplex_policy="throughput")  # bulk round trip: max combined GB/s
     mgr = SwapManager(TransferParams(), bytes_per_block=geo.block_bytes, executor=ex)
-    store = CpuStore(POOL_BLOCKS, reuse_enabled=True)
+    store = CpuStore(HOST_POOL_BLOCKS, reuse_enabled=True)
     n_req, per = 64, PLAN_BLOCKS // 64
     rng = np.random.default_rng(7)
-    runs = random_runs(rng, PLAN_BLOCKS, args.group, POOL_BLOCKS, POOL_BLOCKS)
+    runs = random_runs(rng, PLAN_BLOCKS, args.group, POOL_BLOCKS, HOST_POOL_BLOCKS)
     tables, cursor = [], 0
     per_runs = per // args.group if per >= args.group else 1
     for r in range(n_req):
@@ -450,13 +451,17 @@ def run_trace(args, geo, dev):
         rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, device=dev,
                      copy_impl=impl, timing=True)
         eng = LiveEngine(cfg, generate(wl), rt, decode)
+        eng.turn_trace = []
         rep = eng.run()
         lat = eng.latency_summary()
+        anat = eng.ttft_anatomy()
         st = rt.stats()
         out["runs"][name] = {"ablation": mode, "copy_impl": impl,
                              **{k: lat[k] for k in ("ttft_p50_ms", "ttft_p99_ms", "tbt_p99_ms",
                                                     "tbt_p999_ms", "decode_stall_frac",
                                                     "swap_induced_decode_stall", "wall_s")},
+                             "ttft_tail_ms": {"turns": anat.get("turns"),
+                                              **anat.get("tail_mean_ms", {})},
                              "tokens": rep.total_tokens,
                              "swap_gib": {"out": round(st["bytes_out"] / 2**30, 2),
                                           "in": round(st["bytes_in"] / 2**30, 2)},
@@ -484,9 +489,10 @@ def serving_interference(dp, dev, s):
     s2 = torch.cuda.Stream(device=dev)
     rng = np.random.default_rng(5)
     n = 1024
-    ops = random_runs(rng, n, 16, POOL_BLOCKS // 2, POOL_BLOCKS // 2).astype(np.int32)
+    ops = random_runs(rng, n, 16, POOL_BLOCKS // 2, HOST_POOL_BLOCKS // 2).astype(np.int32)
     ops_in = ops.copy()
-    ops_in[:, 1:] += POOL_BLOCKS // 2
+    ops_in[:, 1] += POOL_BLOCKS // 2
+    ops_in[:, 2] += HOST_POOL_BLOCKS // 2
     nbytes = n * dp.geometry.block_bytes
 
     def steps(k):
@@ -573,7 +579,7 @@ def group_sweep(dp, s):
     rng = np.random.default_rng(11)
     nbytes = PLAN_BLOCKS * geo.block_bytes
     for g in (1, 4, 16, 64, 256):
-        ops = random_runs(rng, PLAN_BLOCKS, g, POOL_BLOCKS, POOL_BLOCKS).astype(np.int32)
+        ops = random_runs(rng, PLAN_BLOCKS, g, POOL_BLOCKS, HOST_POOL_BLOCKS).astype(np.int32)
         row = {"group": g}
         for d in ("out", "in"):
             for impl, fn in (("kernel", lambda: dp.swap(d, ops, stream=s)),

@@ -16,6 +16,7 @@ ROOT = PKG.parent
 LIB_PATH = PKG / "libkvswap.so"
 CU_SRC = PKG / "csrc" / "kvswap.cu"
 HDR = ROOT / "include" / "kvswap.h"
+HDR_WL = ROOT / "include" / "kvswap_workload.h"
 
 ARCH_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -36,7 +37,7 @@ def _stale(target: Path, *deps: Path) -> bool:
 
 def build_kvswap(force: bool = False, verbose: bool = False) -> Path:
     """Compile csrc/kvswap.cu into PKG/libkvswap.so for sm_100a (static cudart)."""
-    if not force and not _stale(LIB_PATH, CU_SRC, HDR, Path(__file__)):
+    if not force and not _stale(LIB_PATH, CU_SRC, HDR, HDR_WL, Path(__file__)):
         return LIB_PATH
     tmp = LIB_PATH.with_suffix(".so.tmp")
     cmd = [

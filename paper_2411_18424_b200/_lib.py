@@ -56,6 +56,7 @@ EXPORTED_SYMBOLS = (
     "kvs_host_alloc",
     "kvs_host_free",
     "kvs_stream_read",  # include/kvswap_workload.h
+    "kvs_kv_tokens",  # include/kvswap_workload.h
 )
 
 DIRECTIONS = {"out": KVS_DIR_OUT, "in": KVS_DIR_IN}
@@ -132,6 +133,9 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_stream_read.restype = c.c_int
     lib.kvs_stream_read.argtypes = [c.c_int, c.c_uint64, c.c_void_p, c.c_size_t, c.c_size_t,
                                     c.c_int, c.c_void_p]
+    lib.kvs_kv_tokens.restype = c.c_int
+    lib.kvs_kv_tokens.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_int32,
+                                  c.c_uint64, c.c_void_p]
 
 
 def load(path: Optional[os.PathLike] = None) -> ctypes.CDLL:

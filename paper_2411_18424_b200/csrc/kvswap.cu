@@ -26,12 +26,14 @@
 #include <unistd.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
 
 #include "kvswap.h"
+#include "kvswap_workload.h"
 
 namespace {
 
@@ -71,6 +73,7 @@ struct SwapParams {
   unsigned long long* bucket;  // shared (both directions) budget clock, ns
   uint64_t bucket_cost_ns;     // >0: ns of budget one piece consumes
   uint64_t bucket_burst_ns;    // idle credit cap
+  uint32_t hint;               // host-side access variant (ld_host / st_host)
   int32_t op_end[CAP];         // inclusive prefix sum of TransferOp.blocks
   int32_t op_gpu[CAP];         // TransferOp.gpu_start
   int32_t op_cpu[CAP];         // TransferOp.cpu_start
@@ -88,6 +91,39 @@ __device__ __forceinline__ void st_plain(void* p, const int4& v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
                "r"(v.z), "r"(v.w)
                : "memory");
+}
+
+// Host-side access variants (KVS_HINT_IN / KVS_HINT_OUT, experiment knob).
+__device__ __forceinline__ int4 ld_host(const void* p, uint32_t hint) {
+  int4 v;
+  if (hint == 1) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  } else if (hint == 2) {
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  } else if (hint == 3) {
+    asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  } else {
+    v = ld_stream(p);
+  }
+  return v;
+}
+
+__device__ __forceinline__ void st_host(void* p, const int4& v, uint32_t hint) {
+  if (hint == 1) {
+    asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w) : "memory");
+  } else if (hint == 2) {
+    asm volatile("st.global.wt.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w) : "memory");
+  } else if (hint == 3) {
+    asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+  } else {
+    st_plain(p, v);
+  }
 }
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -202,11 +238,17 @@ __global__ void __launch_bounds__(kMaxThreads)
     const uint32_t lo = lane * kVecBytes;
 
     int4 v[kUnroll];
+    const uint32_t hint = p.hint;
     if (remain >= kPieceBytes) {
 #pragma unroll
-      for (int j = 0; j < kUnroll; ++j) v[j] = ld_stream(src + j * kWarpBytes + lo);
+      for (int j = 0; j < kUnroll; ++j)
+        v[j] = DIR == KVS_DIR_IN ? ld_host(src + j * kWarpBytes + lo, hint)
+                                 : ld_stream(src + j * kWarpBytes + lo);
 #pragma unroll
-      for (int j = 0; j < kUnroll; ++j) st_plain(dst + j * kWarpBytes + lo, v[j]);
+      for (int j = 0; j < kUnroll; ++j) {
+        if (DIR == KVS_DIR_OUT) st_host(dst + j * kWarpBytes + lo, v[j], hint);
+        else st_plain(dst + j * kWarpBytes + lo, v[j]);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < kUnroll; ++j)
@@ -440,6 +482,7 @@ struct KvsHandle {
   uint64_t pace_ps[2] = {0, 0};  // per 4 KiB piece; 0 = unpaced
   double budget_gbps = 0.0;      // shared by both directions; 0 = none
   unsigned long long* d_bucket = nullptr;
+  uint32_t hint[2] = {0, 0};     // host access variant per direction (env KVS_HINT_OUT/IN)
   int64_t launches = 0;
 };
 
@@ -529,6 +572,7 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
       h->budget_gbps > 0.0 ? static_cast<uint64_t>(piece / h->budget_gbps + 0.5) : 0;
   if (p.bucket_cost_ns == 0 && h->budget_gbps > 0.0) p.bucket_cost_ns = 1;
   p.bucket_burst_ns = 16 * p.bucket_cost_ns;
+  p.hint = h->hint[dir];
   if (o.op_flags != nullptr) {
     // Same stream as the kernel: ordered before it, and after the previous
     // launch of this direction that used the counters.
@@ -636,6 +680,8 @@ int kvs_create(int device, const KvsGeometry* geo, const uint64_t* plane_ptrs, v
   h->num_cpu_blocks = num_cpu_blocks;
   h->host = static_cast<char*>(host_base);
   h->h_planes.assign(plane_ptrs, plane_ptrs + geo->num_planes);
+  if (const char* e = getenv("KVS_HINT_OUT")) h->hint[KVS_DIR_OUT] = static_cast<uint32_t>(atoi(e));
+  if (const char* e = getenv("KVS_HINT_IN")) h->hint[KVS_DIR_IN] = static_cast<uint32_t>(atoi(e));
   rc = cuda_rc(cudaMalloc(&h->d_planes, sizeof(uint64_t) * geo->num_planes));
   if (!rc)
     rc = cuda_rc(cudaMemcpy(h->d_planes, plane_ptrs, sizeof(uint64_t) * geo->num_planes,
@@ -977,4 +1023,121 @@ extern "C" int kvs_stream_read(int device, uint64_t stream, const void* buf, siz
   kvs_stream_read_kernel<<<ctas, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       static_cast<const int4*>(buf), buf_bytes / 16, bytes / 16, static_cast<int4*>(sink));
   return cuda_rc(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic KV producer / checker (include/kvswap_workload.h): what attention
+// would write into the paged cache for each produced token, as one launch
+// with no temporaries (the torch formulation allocated ~n_tokens x 256 KiB of
+// int64 intermediates per iteration).
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int kTokSegsMax = 256;
+
+struct TokSegs {
+  const uint64_t* planes;
+  int64_t stride;          // plane_block_stride
+  uint32_t num_planes;
+  uint32_t block_tokens;
+  uint32_t words;          // int32 words per (K or V) token row
+  uint32_t n_segs;
+  uint32_t* mismatch;      // mode 1: count of mismatching words
+  int32_t mode;            // 0 write, 1 check
+  uint32_t seg_req[kTokSegsMax];
+  int32_t seg_lo[kTokSegsMax];     // first token
+  int32_t seg_tok_end[kTokSegsMax];  // inclusive prefix sum of tokens
+  int32_t seg_phys[kTokSegsMax];   // physical block of token seg_lo
+};
+
+// Runtime._pattern restated in uint32 (identical mod 2^32).
+__device__ __forceinline__ uint32_t kv_word(uint32_t req, uint32_t tok, uint32_t plane,
+                                            uint32_t kv, uint32_t w) {
+  return tok * 0x01000193u + req * 0x5BD1E995u + plane * 0x9E3779B1u + kv * 0x7F4A7C15u + w;
+}
+
+// One warp per (token, plane, kv) row; lanes stride the row's words.
+__global__ void __launch_bounds__(256) kvs_kv_tokens_kernel(const __grid_constant__ TokSegs s) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t total_tokens = static_cast<uint32_t>(s.seg_tok_end[s.n_segs - 1]);
+  const uint64_t rows = static_cast<uint64_t>(total_tokens) * s.num_planes * 2u;
+  uint32_t bad = 0;
+  uint32_t seg = 0;
+  for (uint64_t r = warp; r < rows; r += nwarps) {
+    const uint32_t kv = static_cast<uint32_t>(r & 1u);
+    const uint64_t rp = r >> 1;
+    const uint32_t plane = static_cast<uint32_t>(rp % s.num_planes);
+    const uint32_t i = static_cast<uint32_t>(rp / s.num_planes);  // flat token index
+    while (static_cast<int32_t>(i) >= s.seg_tok_end[seg]) ++seg;
+    const int32_t seg_begin = seg == 0 ? 0 : s.seg_tok_end[seg - 1];
+    const uint32_t tok = static_cast<uint32_t>(s.seg_lo[seg] + (static_cast<int32_t>(i) - seg_begin));
+    const uint32_t blk = s.seg_phys[seg] + tok / s.block_tokens -
+                         static_cast<uint32_t>(s.seg_lo[seg]) / s.block_tokens;
+    const uint32_t slot = tok % s.block_tokens;
+    uint32_t* row = reinterpret_cast<uint32_t*>(
+        reinterpret_cast<char*>(__ldg(s.planes + plane)) + static_cast<int64_t>(blk) * s.stride) +
+        (static_cast<uint64_t>(kv) * s.block_tokens + slot) * s.words;
+    const uint32_t base = kv_word(s.seg_req[seg], tok, plane, kv, 0);
+    if (s.mode == 0) {
+      for (uint32_t w = lane; w < s.words; w += 32) row[w] = base + w;
+    } else {
+      for (uint32_t w = lane; w < s.words; w += 32) bad += row[w] != base + w;
+    }
+  }
+  if (s.mode == 1) {
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if (lane == 0 && bad) atomicAdd(s.mismatch, bad);
+  }
+}
+
+}  // namespace
+
+extern "C" int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_t n_segs,
+                             int32_t block_tokens, uint64_t stream, uint32_t* mismatch) {
+  if (h == nullptr || (mode != 0 && mode != 1) || n_segs < 0 || block_tokens < 1 ||
+      (n_segs > 0 && segs == nullptr) || (mode == 1 && mismatch == nullptr))
+    return KVS_ERR_INVALID;
+  const int64_t chunk = h->geo.plane_chunk_bytes;
+  if (chunk % (2 * block_tokens * 4)) return KVS_ERR_INVALID;
+  int rc = cuda_rc(cudaSetDevice(h->device));
+  if (rc) return rc;
+  auto st = reinterpret_cast<cudaStream_t>(stream);
+  for (int32_t base = 0; base < n_segs; base += kTokSegsMax) {
+    TokSegs s{};
+    s.planes = h->d_planes;
+    s.stride = h->geo.plane_block_stride;
+    s.num_planes = static_cast<uint32_t>(h->geo.num_planes);
+    s.block_tokens = static_cast<uint32_t>(block_tokens);
+    s.words = static_cast<uint32_t>(chunk / (2 * block_tokens * 4));
+    s.mismatch = mismatch;
+    s.mode = mode;
+    int64_t tokens = 0;
+    uint32_t n = 0;
+    for (int32_t i = base; i < n_segs && n < kTokSegsMax; ++i) {
+      const int64_t req = segs[4 * i], lo = segs[4 * i + 1], hi = segs[4 * i + 2],
+                    phys = segs[4 * i + 3];
+      if (req < 0 || lo < 0 || hi < lo || phys < 0) return KVS_ERR_INVALID;
+      if (hi == lo) continue;
+      const int64_t last = phys + (hi - 1) / block_tokens - lo / block_tokens;
+      if (last >= h->num_gpu_blocks) return KVS_ERR_RANGE;
+      tokens += hi - lo;
+      if (tokens > INT32_MAX / 64) return KVS_ERR_RANGE;
+      s.seg_req[n] = static_cast<uint32_t>(req);
+      s.seg_lo[n] = static_cast<int32_t>(lo);
+      s.seg_tok_end[n] = static_cast<int32_t>(tokens);
+      s.seg_phys[n] = static_cast<int32_t>(phys);
+      ++n;
+    }
+    if (n == 0) continue;
+    s.n_segs = n;
+    const uint64_t rows = static_cast<uint64_t>(tokens) * s.num_planes * 2;
+    const uint64_t want = (rows + 7) / 8;  // 8 warps per CTA
+    const int ctas = static_cast<int>(want < 1184 ? want : 1184);
+    kvs_kv_tokens_kernel<<<ctas, 256, 0, st>>>(s);
+    rc = cuda_rc(cudaGetLastError());
+    if (rc) return rc;
+  }
+  return KVS_OK;
 }

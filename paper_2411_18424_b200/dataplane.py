@@ -221,6 +221,17 @@ class SwapDataPlane:
                                           _stream_handle(stream))
         _lib.check(rc, f"kvs_memcpy_baseline({direction}, mode={mode})")
 
+    def kv_tokens(self, mode: int, segs: np.ndarray, stream: Optional[torch.cuda.Stream] = None,
+                  mismatch_ptr: int = 0) -> None:
+        """Write (mode 0) or check (mode 1) the synthetic KV of token segments
+        int64 [n, 4] = (request, lo, hi, physical block of token lo)."""
+        arr = np.ascontiguousarray(segs, dtype=np.int64).reshape(-1, 4)
+        rc = self.lib.kvs_kv_tokens(self.handle, mode, arr.ctypes.data_as(ctypes.c_void_p),
+                                    arr.shape[0], self.geometry.block_tokens,
+                                    _stream_handle(stream),
+                                    ctypes.c_void_p(mismatch_ptr) if mismatch_ptr else None)
+        _lib.check(rc, "kvs_kv_tokens")
+
     def wait_flag(self, stream: Optional[torch.cuda.Stream], flag_ptr: int, value: int) -> None:
         _lib.check(self.lib.kvs_wait_flag(_stream_handle(stream), ctypes.c_void_p(flag_ptr),
                                           value & 0xFFFFFFFF), "kvs_wait_flag")

@@ -34,6 +34,30 @@ class KVIntegrityError(AssertionError):
     """A swapped-in request's KV bytes differ from what its tokens wrote."""
 
 
+def token_segments(spans, extents_of, block_tokens: int) -> np.ndarray:
+    """Token spans [(request, lo, hi)] -> int64 [n, 4] (request, lo, hi,
+    physical block of token lo): one row per physically contiguous stretch of
+    the request's block table `extents_of(request)` = [(start, length)] in
+    logical order (Engine._gpu_extents, engine.py:317-325)."""
+    T = block_tokens
+    rows = []
+    for req, lo, hi in spans:
+        if hi <= lo:
+            continue
+        first, last = lo // T, (hi - 1) // T
+        logical = 0
+        for start, n in extents_of(req):
+            b0, b1 = max(first, logical), min(last, logical + n - 1)
+            if b0 <= b1:
+                rows.append((req, max(lo, b0 * T), min(hi, (b1 + 1) * T), start + b0 - logical))
+            logical += n
+            if logical > last:
+                break
+        if logical <= last:
+            raise IndexError(f"request {req}: tokens up to {hi} exceed its block table")
+    return np.asarray(rows, dtype=np.int64).reshape(-1, 4)
+
+
 class Runtime:
     def __init__(self, geometry: KVGeometry, gpu_blocks: int, cpu_blocks: int,
                  device="cuda:0", copy_impl: str = "kernel", write_kv: bool = True,
@@ -67,53 +91,35 @@ class Runtime:
             1, 1, -1, 1)
         self._word_term = torch.arange(self._words, device=dev, dtype=torch.int64).view(
             1, 1, 1, -1)
+        self._mismatch = torch.zeros(1, dtype=torch.int32, device=dev)
 
     # -- token KV pattern -----------------------------------------------------
 
     def _pattern(self, reqs: torch.Tensor, tokens: torch.Tensor) -> torch.Tensor:
-        """int32 [n, P, 2, words]: deterministic KV of each (request, token)."""
+        """int32 [n, P, 2, words]: the deterministic KV of each (request, token)
+        that kvs_kv_tokens writes (torch restatement, used by tests)."""
         base = (tokens * 0x01000193 + reqs * 0x5BD1E995).view(-1, 1, 1, 1)
         v = (base + self._plane_term + self._kv_term + self._word_term) & 0xFFFFFFFF
         return (v - ((v >> 31) << 32)).to(torch.int32)
 
-    def _slots_of(self, engine, spans):
-        """Flattened (request, token, physical block, slot) for token spans."""
-        T = self.geometry.block_tokens
-        reqs, toks, phys = [], [], []
-        for req, lo, hi in spans:
-            if hi <= lo:
-                continue
-            table = np.concatenate([np.arange(s, s + n) for s, n in engine._gpu_extents(req)])
-            t = np.arange(lo, hi, dtype=np.int64)
-            reqs.append(np.full(hi - lo, req, dtype=np.int64))
-            toks.append(t)
-            phys.append(table[t // T])
-        if not toks:
-            return None
-        dev = self.cache.device
-        r = torch.from_numpy(np.concatenate(reqs)).to(dev, non_blocking=True)
-        t = torch.from_numpy(np.concatenate(toks)).to(dev, non_blocking=True)
-        p = torch.from_numpy(np.concatenate(phys)).to(dev, non_blocking=True)
-        return r, t, p, t % T
+    def segments(self, engine, spans) -> np.ndarray:
+        return token_segments(spans, engine._gpu_extents, self.geometry.block_tokens)
 
     # -- engine hooks ------------------------------------------------------------
 
     def compute(self, engine, spans) -> None:
         """One iteration's compute on the compute stream: wait for conflicting
-        transfers, then write the KV of every produced token (one scatter)."""
+        transfers, then write the KV of every produced token (one launch)."""
         extents = []
         for req, _, _ in spans:
             extents.extend(engine._gpu_extents(req))
         self.barrier_waits += self.executor.compute_barrier(extents)
         if not self.write_kv:
             return
-        with torch.cuda.stream(self.executor.compute):
-            got = self._slots_of(engine, spans)
-            if got is None:
-                return
-            r, t, p, slot = got
-            self._slots[:, p, :, slot, :] = self._pattern(r, t)
-            self.tokens_written += int(t.numel())
+        segs = self.segments(engine, spans)
+        if len(segs):
+            self.dataplane.kv_tokens(0, segs, stream=self.executor.compute)
+            self.tokens_written += int((segs[:, 2] - segs[:, 1]).sum())
 
     def swap_in_landed(self, engine, req: int) -> None:
         if not self.verify:
@@ -123,13 +129,16 @@ class Runtime:
         if valid <= 0:
             return
         self.executor.compute_barrier(engine._gpu_extents(req))
+        segs = self.segments(engine, [(req, 0, valid)])
         with torch.cuda.stream(self.executor.compute):
-            r, t, p, slot = self._slots_of(engine, [(req, 0, valid)])
-            got = self._slots[:, p, :, slot, :]
-            bad = int((got != self._pattern(r, t)).any(dim=(1, 2, 3)).sum().item())
+            self._mismatch.zero_()
+        self.dataplane.kv_tokens(1, segs, stream=self.executor.compute,
+                                 mismatch_ptr=self._mismatch.data_ptr())
+        self.executor.compute.synchronize()
+        bad = int(self._mismatch.item())
         if bad:
             raise KVIntegrityError(
-                f"request {req}: {bad} of {valid} tokens' KV differ after swap-in "
+                f"request {req}: {bad} KV words of its {valid} tokens differ after swap-in "
                 f"(iteration {engine.iteration})")
         self.verified += 1
 

@@ -122,3 +122,47 @@ def test_live_engine_bytes_and_latency(cuda_ok):
     assert lat["ttft_p99_ms"] is not None and lat["tbt_p99_ms"] > 0
     assert dec.bytes_per_us > 1e6  # > 1 TB/s calibrated weight streaming
     rt.close()
+
+
+@pytest.mark.parametrize("geo_name", ["tiny", "llama3-8b"])
+def test_kv_token_kernel_matches_torch_pattern(cuda_ok, geo_name):
+    """kvs_kv_tokens (write + check) against the plain torch restatement."""
+    import numpy as np
+    import torch
+
+    from paper_2411_18424_b200.geometry import PRESETS
+    from paper_2411_18424_b200.runtime import Runtime, token_segments
+
+    geo = TINY if geo_name == "tiny" else PRESETS[geo_name]
+    G = 64
+    rt = Runtime(geo, G, 8, verify=True)
+    rt.cache.planes.fill_(0)
+    T = geo.block_tokens
+    tables = {3: [(40, 3), (5, 2)], 9: [(20, 4)], 123456: [(60, 4)]}
+    spans = [(3, 7, 70), (9, 0, 64), (123456, 17, 18)]
+    segs = token_segments(spans, tables.__getitem__, T)
+    s = rt.executor.compute
+    rt.dataplane.kv_tokens(0, segs, stream=s)
+    s.synchronize()
+    want = torch.zeros_like(rt._slots)
+    for req, lo, hi in spans:
+        flat = [b for st, n in tables[req] for b in range(st, st + n)]
+        t = torch.arange(lo, hi, device=want.device)
+        p = torch.tensor([flat[x // T] for x in range(lo, hi)], device=want.device)
+        r = torch.full_like(t, req)
+        want[:, p, :, t % T, :] = rt._pattern(r, t)
+    assert torch.equal(rt._slots, want)
+    # check mode: exact -> 0; one flipped word -> counted
+    rt._mismatch.zero_()
+    rt.dataplane.kv_tokens(1, segs, stream=s, mismatch_ptr=rt._mismatch.data_ptr())
+    s.synchronize()
+    assert int(rt._mismatch.item()) == 0
+    rt._slots[1, 41, 1, 3, 0] ^= 1  # req 3, token 19 -> block 41 slot 3, plane 1, V
+    torch.cuda.synchronize()
+    rt._mismatch.zero_()
+    rt.dataplane.kv_tokens(1, segs, stream=s, mismatch_ptr=rt._mismatch.data_ptr())
+    s.synchronize()
+    assert int(rt._mismatch.item()) == 1
+    with pytest.raises(IndexError):
+        rt.dataplane.kv_tokens(0, np.array([[0, 0, 32, G - 1]]), stream=s)
+    rt.close()

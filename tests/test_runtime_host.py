@@ -1,0 +1,52 @@
+"""Host-side logic of the runtime (no GPU): token spans -> KV-write segments."""
+
+import numpy as np
+import pytest
+
+from paper_2411_18424_b200.runtime import token_segments
+
+
+def expand(segs, T):
+    """segments -> {(req, token): (physical block, slot)}"""
+    out = {}
+    for req, lo, hi, phys in segs.tolist():
+        for t in range(lo, hi):
+            out[(req, t)] = (phys + t // T - lo // T, t % T)
+    return out
+
+
+def brute(spans, tables, T):
+    out = {}
+    for req, lo, hi in spans:
+        flat = [b for s, n in tables[req] for b in range(s, s + n)]
+        for t in range(lo, hi):
+            out[(req, t)] = (flat[t // T], t % T)
+    return out
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_segments_match_block_table(seed):
+    rng = np.random.default_rng(seed)
+    T = 16
+    tables, spans = {}, []
+    for req in range(6):
+        n_ext = int(rng.integers(1, 6))
+        starts = rng.choice(1000, size=n_ext, replace=False) * 8
+        tables[req] = [(int(s), int(rng.integers(1, 8))) for s in starts]
+        cap = sum(n for _, n in tables[req]) * T
+        lo = int(rng.integers(0, cap))
+        hi = int(rng.integers(lo, cap + 1))
+        spans.append((req, lo, hi))
+    segs = token_segments(spans, tables.__getitem__, T)
+    assert expand(segs, T) == brute(spans, tables, T)
+    # each segment stays inside one physically contiguous extent
+    for req, lo, hi, phys in segs.tolist():
+        last = phys + (hi - 1) // T - lo // T
+        assert any(s <= phys and last < s + n for s, n in tables[req])
+
+
+def test_empty_and_overflowing_spans():
+    tables = {0: [(10, 2)]}
+    assert token_segments([(0, 5, 5)], tables.__getitem__, 16).shape == (0, 4)
+    with pytest.raises(IndexError):
+        token_segments([(0, 0, 33)], tables.__getitem__, 16)

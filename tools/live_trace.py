@@ -38,6 +38,7 @@ def run_one(args, mode, impl, decode, geo):
     rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, copy_impl=impl,
                  verify=args.verify, timing=True, duplex_policy=args.policy)
     eng = LiveEngine(cfg, generate(wl), rt, decode)
+    eng.turn_trace = []
     t0 = time.perf_counter()
     rep = eng.run()
     wall = time.perf_counter() - t0
@@ -66,6 +67,7 @@ def run_one(args, mode, impl, decode, geo):
             reverse=True)[:8],
         "slowest_iterations": sorted(eng._trace, reverse=True)[:8],
         "ttft_top": sorted(eng.ttft_samples, reverse=True)[:8],
+        "ttft_anatomy": eng.ttft_anatomy(),
     }
     rt.close()
     return out
@@ -96,8 +98,7 @@ def main():
         res = run_one(args, mode, impl, decode, geo)
         results["runs"].append(res)
         print(json.dumps({k: res[k] for k in ("mode", "copy_impl", "wall_s", "latency", "swap",
-                                              "slowest_transfers_ms", "slowest_iterations",
-                                              "ttft_top")}),
+                                              "slowest_transfers_ms", "ttft_anatomy")}),
               flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
