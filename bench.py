@@ -230,7 +230,8 @@ def run_ours(args, geo):
     import torch
     import torch.distributed as dist
 
-    from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
+    from paper_2411_18424_b200.dataplane import (HostKVPool, PagedKVCache, SwapDataPlane,
+                                                 numa_nodes)
 
     rank, world, local = dist_env()
     if not torch.cuda.is_available():
@@ -241,7 +242,8 @@ def run_ours(args, geo):
         dist.init_process_group("nccl", device_id=dev)
 
     cache = PagedKVCache(geo, POOL_BLOCKS, device=dev)
-    host = HostKVPool(HOST_POOL_BLOCKS, geo.block_bytes)
+    host = HostKVPool(HOST_POOL_BLOCKS, geo.block_bytes, numa_node=None, device=dev)
+    host_numa = host.numa_node
     dp = SwapDataPlane(cache, host, ctas={"out": args.ctas, "in": args.ctas})
     cache.planes.view(torch.int32).random_()
     out_ops, in_ops = make_plans(args.group, seed=rank)
@@ -337,7 +339,9 @@ def run_ours(args, geo):
                        "model_kv": geo.name, "block_bytes": geo.block_bytes,
                        "plan_blocks": PLAN_BLOCKS, "group_blocks": args.group,
                        "parallelism": f"replicas{world} (per-rank KV shard, own PCIe link)",
-                       "l2": "inputs 8 GiB/direction > 126 MB L2, no flush"},
+                       "l2": "inputs 8 GiB/direction > 126 MB L2, no flush",
+                       "host_pool": {"blocks": HOST_POOL_BLOCKS, "numa_node": host_numa,
+                                     "numa_nodes": numa_nodes()}},
             "per_direction_gbs": {"out": round(out_gbs, 3), "in": round(in_gbs, 3)},
             "roofline": {"bound": "pcie", "achieved": round(achieved, 3),
                          "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",

@@ -20,8 +20,10 @@ extern "C" {
 #endif
 
 /* Stream-read `bytes` of device memory of `device` starting at `buf`
- * (wrapping over `buf_bytes`), on `stream`, with `ctas` CTAs (0 = 2 x SM
- * count).  `sink` (device, 16 B) receives a value only the compiler cannot
+ * (wrapping over `buf_bytes`), on `stream`, with `ctas` persistent CTAs
+ * (0 = 2 x SM count; each CTA owns a fixed 1/ctas share, so the step is as
+ * slow as its slowest SM), or, for ctas < 0, one CTA per -ctas KiB tile
+ * (thousands of CTAs that the block scheduler balances across SMs).  `sink` (device, 16 B) receives a value only the compiler cannot
  * prove dead.  Returns 0, a KVS_ERR_* code or a cudaError_t. */
 int kvs_stream_read(int device, uint64_t stream, const void* buf, size_t buf_bytes,
                     size_t bytes, int ctas, void* sink);

@@ -1005,12 +1005,58 @@ __global__ void __launch_bounds__(512) kvs_stream_read_kernel(const int4* __rest
   if (acc == 0x9E3779B9u) sink->x = static_cast<int>(acc);  // practically never
 }
 
+// Tiled variant: CTA b streams tile b (tile_vecs 16-B vectors) of the bytes;
+// many more CTAs than SMs, so the hardware block scheduler balances the SMs
+// (how a weight-streaming GEMV is usually tiled: one CTA per weight tile).
+__global__ void __launch_bounds__(512) kvs_stream_read_tiled_kernel(const int4* __restrict__ buf,
+                                                                    uint64_t buf_vecs,
+                                                                    uint64_t total_vecs,
+                                                                    uint64_t tile_vecs,
+                                                                    int4* sink) {
+  const bool pow2 = (buf_vecs & (buf_vecs - 1)) == 0;
+  const uint64_t mask = buf_vecs - 1;
+  const uint64_t lo = blockIdx.x * tile_vecs;
+  const uint64_t hi = lo + tile_vecs < total_vecs ? lo + tile_vecs : total_vecs;
+  uint32_t acc = 0;
+  uint64_t i = lo + threadIdx.x;
+  const uint64_t step = blockDim.x;
+  for (; i + 3 * step < hi; i += 4 * step) {
+    int4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t x = i + j * step;
+      v[j] = ld_stream(buf + (pow2 ? (x & mask) : (x % buf_vecs)));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc ^= v[j].x ^ v[j].y ^ v[j].z ^ v[j].w;
+  }
+  for (; i < hi; i += step) {
+    const int4 v = ld_stream(buf + (pow2 ? (i & mask) : (i % buf_vecs)));
+    acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9E3779B9u) sink->x = static_cast<int>(acc);
+}
+
 }  // namespace
 
 extern "C" int kvs_stream_read(int device, uint64_t stream, const void* buf, size_t buf_bytes,
                                size_t bytes, int ctas, void* sink) {
-  if (buf == nullptr || sink == nullptr || buf_bytes < 16 || bytes == 0 || ctas < 0 || device < 0)
+  if (buf == nullptr || sink == nullptr || buf_bytes < 16 || bytes == 0 || device < 0)
     return KVS_ERR_INVALID;
+  if (ctas < 0) {  // tiled: -ctas KiB per CTA
+    if (reinterpret_cast<uintptr_t>(buf) % 16 || reinterpret_cast<uintptr_t>(sink) % 16)
+      return KVS_ERR_ALIGN;
+    int rc = cuda_rc(cudaSetDevice(device));
+    if (rc) return rc;
+    const uint64_t tile_vecs = static_cast<uint64_t>(-static_cast<int64_t>(ctas)) * 1024 / 16;
+    const uint64_t total = bytes / 16;
+    const uint64_t grid = (total + tile_vecs - 1) / tile_vecs;
+    if (grid > 0x7FFFFFFFull) return KVS_ERR_RANGE;
+    kvs_stream_read_tiled_kernel<<<static_cast<unsigned>(grid), 512, 0,
+                                   reinterpret_cast<cudaStream_t>(stream)>>>(
+        static_cast<const int4*>(buf), buf_bytes / 16, total, tile_vecs, static_cast<int4*>(sink));
+    return cuda_rc(cudaGetLastError());
+  }
   if (reinterpret_cast<uintptr_t>(buf) % 16 || reinterpret_cast<uintptr_t>(sink) % 16)
     return KVS_ERR_ALIGN;
   int rc = cuda_rc(cudaSetDevice(device));

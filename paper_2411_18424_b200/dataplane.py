@@ -50,14 +50,50 @@ def _stream_handle(stream: Optional[torch.cuda.Stream]) -> int:
     return int(stream.cuda_stream)
 
 
-class HostKVPool:
-    """Pinned, device-mapped host swap space: [num_blocks, block_bytes] bytes."""
+def numa_nodes() -> int:
+    """Number of online NUMA nodes of this host (1 when unknown)."""
+    try:
+        with open("/sys/devices/system/node/online") as f:
+            spec = f.read().strip()
+    except OSError:
+        return 1
+    n = 0
+    for part in spec.split(","):
+        lo, _, hi = part.partition("-")
+        n += int(hi or lo) - int(lo) + 1
+    return max(1, n)
 
-    def __init__(self, num_blocks: int, block_bytes: int, numa_node: int = -1,
-                 register: bool = False) -> None:
+
+def gpu_numa_node(device: Union[int, str, torch.device, None]) -> int:
+    """NUMA node of the GPU's PCIe root (sysfs), or -1 when unknown.  Each
+    rank's swap space belongs on its own GPU's socket: host-link traffic then
+    never crosses the inter-socket fabric."""
+    try:
+        idx = torch.device(device if device is not None else "cuda").index
+        props = torch.cuda.get_device_properties(idx if idx is not None else 0)
+        bdf = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bdf}/numa_node") as f:
+            return int(f.read().strip())
+    except (OSError, ValueError, RuntimeError, AssertionError):
+        return -1
+
+
+class HostKVPool:
+    """Pinned, device-mapped host swap space: [num_blocks, block_bytes] bytes.
+
+    numa_node=None with a `device` places the pool on that GPU's NUMA node
+    (mmap + mbind + cudaHostRegister) on multi-socket hosts; single-node hosts
+    use cudaHostAlloc."""
+
+    def __init__(self, num_blocks: int, block_bytes: int, numa_node: Optional[int] = -1,
+                 register: bool = False, device=None) -> None:
         if num_blocks < 1 or block_bytes < 16 or block_bytes % 16:
             raise ValueError("host pool needs >= 1 block of a 16-byte multiple")
         lib = _lib.load()
+        if numa_node is None:
+            numa_node = gpu_numa_node(device) if numa_nodes() > 1 else -1
+            register = register or numa_node >= 0
+        self.numa_node = numa_node
         self.num_blocks = num_blocks
         self.block_bytes = block_bytes
         self.nbytes = num_blocks * block_bytes

@@ -67,7 +67,7 @@ class Runtime:
             raise ValueError("runtime token writes assume fused K/V planes")
         self.geometry = geometry
         self.cache = PagedKVCache(geometry, gpu_blocks, device=device)
-        self.host = HostKVPool(cpu_blocks, geometry.block_bytes)
+        self.host = HostKVPool(cpu_blocks, geometry.block_bytes, numa_node=None, device=device)
         self.dataplane = SwapDataPlane(self.cache, self.host)
         self.executor = StreamExecutor(self.dataplane, copy_impl=copy_impl, timing=timing,
                                        duplex_policy=duplex_policy)

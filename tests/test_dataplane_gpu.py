@@ -204,6 +204,7 @@ def test_config1_round_trip_llama3_8b(cuda_ok, path):
     cpu_tab = orc.random_block_table(rng, total, C)
     bounds = np.concatenate([[0], np.cumsum(foot)])
     original = cache.planes[:, torch.from_numpy(gpu_tab).cuda()].clone()
+    torch.cuda.synchronize()  # the KV fill runs on torch's stream, the swaps on s_out
     s_out, s_in = torch.cuda.Stream(), torch.cuda.Stream()
     for r in range(64):
         lo, hi = bounds[r], bounds[r + 1]
@@ -369,6 +370,7 @@ def test_pacing_and_shared_budget(cuda_ok, path):
     cache, host, dp = _mk(torch, LLAMA3_8B, G, C, path=path)
     gen = torch.Generator(device="cuda:0").manual_seed(1)
     cache.planes.view(torch.int32).random_(generator=gen)
+    torch.cuda.synchronize()  # the fill runs on torch's stream, the swaps on s1 / s2
     rng = np.random.default_rng(9)
     ops = orc.random_runs(rng, 256, 16, G // 2, C // 2)  # 512 MiB
     ops_in = ops.copy()

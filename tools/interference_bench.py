@@ -44,7 +44,8 @@ def main():
     host = HostKVPool(POOL, geo.block_bytes)
     dp = SwapDataPlane(cache, host)
     cache.planes.view(torch.int32).random_()
-    dec = DecodeEmulator("cuda:0", weight_bytes=16 << 30)
+    dec = DecodeEmulator("cuda:0", weight_bytes=16 << 30,
+                         ctas=int(os.environ.get("DECODE_CTAS", "0")))
     comp = torch.cuda.Stream(priority=-1)
     s_out, s_in = torch.cuda.Stream(), torch.cuda.Stream()
     rng = np.random.default_rng(0)
@@ -60,14 +61,35 @@ def main():
     evs = decode_steps(dec, comp, 40)
     torch.cuda.synchronize()
     solo = statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(40))
-    results = {"decode_step_solo_ms": round(solo, 4), "runs": []}
+    results = {"decode_step_solo_ms": round(solo, 4), "decode_ctas": dec.ctas, "runs": []}
     print(json.dumps(results), flush=True)
 
     # (label, path, {dir: (ctas, threads)}, {dir: pace GB/s}, impl, dirs)
     # impl: kernel | ce_batch | ce_per_run
     sweep = os.environ.get("SWEEP", "in")
     configs = []
-    if sweep == "in":
+    if sweep == "probe":
+        for ct, pace in (((148, 32), 20.0), ((148, 32), 40.0), ((148, 32), 50.0),
+                         ((16, 512), 50.0), ((4, 512), 50.0), ((4, 512), 0.0)):
+            configs.append((f"lsu{ct[0]}x{ct[1]}", "lsu", {"out": (8, 512), "in": ct},
+                            {"out": 0.0, "in": pace}, "kernel", ("in",)))
+        configs.append(("ce_per_run", "lsu", {"out": (8, 512), "in": (16, 512)},
+                        {"out": 0.0, "in": 0.0}, "ce_per_run", ("in",)))
+        configs.append(("lsu8x512", "lsu", {"out": (8, 512), "in": (148, 32)},
+                        {"out": 52.0, "in": 0.0}, "kernel", ("out",)))
+        configs.append(("lsu_duplex", "lsu", {"out": (8, 512), "in": (148, 32)},
+                        {"out": 25.0, "in": 25.0}, "kernel", ("out", "in")))
+    elif sweep == "probe2":
+        for ct in ((2, 512), (3, 512), (4, 512), (6, 512), (4, 256), (8, 256), (16, 128)):
+            configs.append((f"lsu{ct[0]}x{ct[1]}", "lsu", {"out": (8, 512), "in": ct},
+                            {"out": 0.0, "in": 0.0}, "kernel", ("in",)))
+        for ct in ((1, 512), (2, 512), (2, 256), (4, 128)):
+            configs.append((f"lsu{ct[0]}x{ct[1]}", "lsu", {"out": ct, "in": (4, 512)},
+                            {"out": 0.0, "in": 0.0}, "kernel", ("out",)))
+        for po in (0.0, 26.0, 30.0):
+            configs.append(("duplex_in4x512", "lsu", {"out": (8, 512), "in": (4, 512)},
+                            {"out": po, "in": 0.0}, "kernel", ("out", "in")))
+    elif sweep == "in":
         for ct in ((16, 512), (32, 128), (64, 64), (148, 32)):
             for pace in (0.0, 48.0, 40.0):
                 configs.append((f"lsu{ct[0]}x{ct[1]}", "lsu", {"out": (8, 512), "in": ct},
@@ -124,7 +146,7 @@ def main():
         dp.set_path(d, "lsu")
         dp.set_pace(d, 0.0)
     os.makedirs("gpurun_out", exist_ok=True)
-    with open("gpurun_out/interference.json", "w") as f:
+    with open(os.environ.get("OUT", "gpurun_out/interference.json"), "w") as f:
         json.dump(results, f, indent=1)
     host.close()
 
