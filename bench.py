@@ -236,10 +236,17 @@ def run_ours(args, geo):
     rank, world, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
+    # KVS_BENCH_BACKEND=gloo lets N ranks share fewer GPUs (a code-path check
+    # of the N>1 bench on a 1-GPU box; its numbers are not a scaling result).
+    backend = os.environ.get("KVS_BENCH_BACKEND", "nccl")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     cache = PagedKVCache(geo, POOL_BLOCKS, device=dev)
     host = HostKVPool(HOST_POOL_BLOCKS, geo.block_bytes, numa_node=None, device=dev)
@@ -438,6 +445,13 @@ def run_trace(args, geo, dev):
     from paper_2411_18424_b200.runtime import Runtime
     from paper_2411_18424_b200.workload import generate
 
+    _, world, _ = dist_env()
+    agreement = None
+    if world > 1:
+        # one TP group: every rank swaps its own KV-head shard, decisions in lockstep
+        from paper_2411_18424_b200.live import RankAgreement
+        geo = geo.with_tp(world)
+        agreement = RankAgreement(device=dev)
     decode = DecodeEmulator(dev, weight_bytes=16 << 30)
     doc = {"block": {"bytes_per_block": geo.block_bytes}, "gpu_pool": {"total_blocks": 512},
            "cpu_pool": {"total_blocks": 4096},
@@ -445,16 +459,17 @@ def run_trace(args, geo, dev):
                         "think_time_mean_s": 2.0},
            "trace": {"pattern": "markov", "frequency": 0.04}}
     out = {"workload": f"{args.trace_convs} conversations, 4 req/s, think 2 s, 512 x "
-                       f"{geo.block_bytes >> 20} MiB GPU blocks, Markov f=0.04, decode = "
-                       f"{decode.bytes_per_us / 1e3:.0f} GB/s weight streaming",
-           "runs": {}}
+                       f"{geo.block_bytes / 2**20:g} MiB GPU blocks per rank (TP{world}), "
+                       f"Markov f=0.04, decode = {decode.bytes_per_us / 1e3:.0f} GB/s weight "
+                       f"streaming per rank",
+           "tp": world, "runs": {}}
     for name, mode, impl in (("fastswitch", "full", "kernel"),
                              ("vllm_like", "baseline", "ce_per_block")):
         cfg, wl, _ = mconfig.build({**doc, "ablation": mode})
         cfg = dataclasses.replace(cfg, transfer=b200_transfer_params())
         rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, device=dev,
                      copy_impl=impl, timing=True)
-        eng = LiveEngine(cfg, generate(wl), rt, decode)
+        eng = LiveEngine(cfg, generate(wl), rt, decode, agreement=agreement)
         eng.turn_trace = []
         rep = eng.run()
         lat = eng.latency_summary()

@@ -117,16 +117,59 @@ class LiveStats:
         return (self.busy_ms / self.busy_nominal_ms) / (self.quiet_ms / self.quiet_nominal_ms) - 1
 
 
+class RankAgreement:
+    """Control-plane agreement of a tensor-parallel group in live mode.
+
+    Every TP rank runs the same engine over its own KV-head shard.  Replay
+    decisions are deterministic, but live ones read the wall clock and poll
+    CUDA events, which differ per rank.  So once per iteration the ranks agree
+    on (a) the clock (max over ranks) and (b) which in-flight swaps have
+    landed (a swap counts only once it landed on every rank): one all_reduce(MIN)
+    over [-clock, landed_0, landed_1, ...].  A second, scalar one agrees on the
+    iteration's end time.  Identical inputs -> identical decisions on every
+    rank; the KV bytes never leave their rank (no collective on the data path).
+    """
+
+    def __init__(self, group=None, device=None) -> None:
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.device = (torch.device(device) if dist.get_backend(group) == "nccl"
+                       else torch.device("cpu"))
+        self.calls = 0
+        self.seconds = 0.0
+
+    def _min(self, values: list[int]) -> list[int]:
+        t0 = time.perf_counter()
+        t = torch.tensor(values, dtype=torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        out = t.tolist()
+        self.calls += 1
+        self.seconds += time.perf_counter() - t0
+        return out
+
+    def clock(self, local_us: int) -> int:
+        return -self._min([-int(local_us)])[0]
+
+    def landed(self, local_us: int, flags: list[bool]) -> tuple[int, list[bool]]:
+        out = self._min([-int(local_us)] + [1 if f else 0 for f in flags])
+        return -out[0], [bool(x) for x in out[1:]]
+
+
 class LiveEngine(Engine):
-    """Engine whose clock, swap completions and compute are real (one GPU)."""
+    """Engine whose clock, swap completions and compute are real (one GPU;
+    with `agreement`, one TP rank of a group that decides in lockstep)."""
 
     def __init__(self, config: EngineConfig, conversations, runtime, decode: DecodeEmulator,
-                 time_scale: float = 1.0) -> None:
+                 time_scale: float = 1.0, agreement: Optional[RankAgreement] = None) -> None:
         if runtime is None:
             raise ValueError("live mode needs a Runtime (real data plane)")
         super().__init__(config, conversations, runtime=runtime)
         self.decode = decode
         self.time_scale = time_scale
+        self.agreement = agreement
         self.live = LiveStats()
         # per computing iteration: (duration_us, cpu_us, wait_ms, kernel_ms,
         #                           synced, conflict_waits, n_prefill, n_decode)
@@ -139,11 +182,28 @@ class LiveEngine(Engine):
 
     # -- step 1 made real ------------------------------------------------------
 
+    def _sync_clock(self) -> int:
+        """This iteration's clock (agreed across the TP group, if any) and,
+        with a group, the agreed landed-set of in-flight swaps."""
+        now = self._now()
+        if self.agreement is None:
+            self._landed = None
+            return now
+        flags = [f.transfer is None or f.transfer.poll() for f in self.manager.in_flight]
+        now, self._landed = self.agreement.landed(now, flags)
+        return now
+
+    def _end_clock(self) -> int:
+        now = self._now()
+        return now if self.agreement is None else self.agreement.clock(now)
+
     def _collect_live(self) -> bool:
         moved = False
         keep = []
-        for f in self.manager.in_flight:
-            if f.transfer is not None and not f.transfer.poll():
+        landed = self._landed
+        for i, f in enumerate(self.manager.in_flight):
+            done = (f.transfer is None or f.transfer.poll()) if landed is None else landed[i]
+            if not done:
                 keep.append(f)
                 continue
             if f.direction == "out":
@@ -215,12 +275,15 @@ class LiveEngine(Engine):
         first_arrival = self.conversations[0].arrival if self.conversations else 0
         ex = self.runtime.executor
         compute = ex.compute
+        if self.agreement is not None:
+            self.agreement.clock(0)  # the TP group starts its clocks together
+        self._landed = None
         self._t0 = time.perf_counter()
         self._skip = first_arrival
         wall0 = time.perf_counter()
 
         while True:
-            self.clock = self._now()
+            self.clock = self._sync_clock()
             self._inject_arrivals()
             if not self._live_ids():
                 if not self._future:
@@ -276,7 +339,7 @@ class LiveEngine(Engine):
             prefillers, decoders, prefill_tokens, recompute, spans = self._assemble_batch()
             if not (prefillers or decoders):
                 self._wait_any(self.infer.decode_base)
-                end = self._now()
+                end = self._end_clock()
                 idle = idle + (0 if progress else 1)
                 if idle >= LIVE_DEADLOCK_ITERATIONS:
                     from .engine import DeadlockError
@@ -295,7 +358,7 @@ class LiveEngine(Engine):
             nbytes = self.decode.launch_us(compute, nominal_us)
             e1.record(compute)
             compute.synchronize()
-            end = self._now()
+            end = self._end_clock()
             kernel_ms = e0.elapsed_time(e1)
             self._trace.append((end - start, int((t_cpu - t_iter) * 1e6), e_pre.elapsed_time(e0),
                                 kernel_ms, decision.mode == "sync" and bool(pending),
@@ -383,4 +446,7 @@ class LiveEngine(Engine):
             "idle_waits": self.live.idle_waits,
             "wall_s": round(self.live.wall_s, 2),
             "slow_iterations": self.spike_breakdown(),
+            "tp_agreement": None if self.agreement is None else {
+                "ranks": self.agreement.world, "calls": self.agreement.calls,
+                "mean_us": round(self.agreement.seconds / max(1, self.agreement.calls) * 1e6, 1)},
         }

@@ -187,14 +187,14 @@ COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 # profiles/r01_duplex_bw.json).  Unpaced, SM stores/loads to host memory are
 # issued far faster than PCIe drains them and back up the XBAR/L2 queues that
 # decode's HBM traffic shares: a concurrent 2 ms decode step slowed 1.2-4.9x.
-# Paced to the link rate the same swaps cost decode ~2% (out) / ~9% (in):
-#   latency    — serving: out 8x512 @52 GB/s, in 148x32 @50 GB/s, both
+# Paced to the link rate the same swaps cost decode ~2-4% (out) / ~9% (in):
+#   latency    — serving: out 8x512 @52 GB/s, in 148x32 @51.5 GB/s, both
 #                directions together capped at 60 GB/s (shared budget);
 #   throughput — bulk migration: unpaced, balanced 32x512 each way
 #                (highest combined GB/s, decode pays for it);
 #   unpaced    — out 8x512, in 32x512, no pacing (round-1 default shape).
 DUPLEX_POLICIES = {
-    "latency": {"out": (8, 512, 52.0), "in": (148, 32, 50.0), "budget": 60.0},
+    "latency": {"out": (8, 512, 52.0), "in": (148, 32, 51.5), "budget": 60.0},
     "throughput": {"out": (32, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
     "unpaced": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
 }

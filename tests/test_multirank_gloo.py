@@ -70,3 +70,43 @@ def test_two_rank_tp_shards_agree_on_plans():
         assert plans > 0
     assert [g[4] for g in got] == [(0, 4), (4, 8)]  # head shards partition 8 KV heads
     assert got[0][6] == got[1][6]
+
+
+def _agree_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2411_18424_b200.live import RankAgreement
+
+        ag = RankAgreement()
+        # rank 1's clock runs ahead; a swap counts as landed only once it landed everywhere
+        flags = [[True, False, True, True], [True, True, False, True]][rank]
+        clock, landed = ag.landed(1000 + 500 * rank, flags)
+        end = ag.clock(7 - rank)
+        empty = ag.landed(3, [])
+        q.put((rank, clock, landed, end, empty, ag.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rank_agreement_max_clock_and_all_landed():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_agree_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, clock, landed, end, empty, calls in got:
+        assert clock == 1500
+        assert landed == [True, False, False, True]
+        assert end == 7
+        assert empty == (3, [])
+        assert calls == 3
