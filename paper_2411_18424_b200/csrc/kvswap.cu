@@ -26,7 +26,6 @@
 #include <unistd.h>
 
 #include <cstdint>
-#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -73,7 +72,6 @@ struct SwapParams {
   unsigned long long* bucket;  // shared (both directions) budget clock, ns
   uint64_t bucket_cost_ns;     // >0: ns of budget one piece consumes
   uint64_t bucket_burst_ns;    // idle credit cap
-  uint32_t hint;               // host-side access variant (ld_host / st_host)
   int32_t op_end[CAP];         // inclusive prefix sum of TransferOp.blocks
   int32_t op_gpu[CAP];         // TransferOp.gpu_start
   int32_t op_cpu[CAP];         // TransferOp.cpu_start
@@ -91,39 +89,6 @@ __device__ __forceinline__ void st_plain(void* p, const int4& v) {
   asm volatile("st.global.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
                "r"(v.z), "r"(v.w)
                : "memory");
-}
-
-// Host-side access variants (KVS_HINT_IN / KVS_HINT_OUT, experiment knob).
-__device__ __forceinline__ int4 ld_host(const void* p, uint32_t hint) {
-  int4 v;
-  if (hint == 1) {
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  } else if (hint == 2) {
-    asm volatile("ld.global.L1::no_allocate.L2::256B.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  } else if (hint == 3) {
-    asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  } else {
-    v = ld_stream(p);
-  }
-  return v;
-}
-
-__device__ __forceinline__ void st_host(void* p, const int4& v, uint32_t hint) {
-  if (hint == 1) {
-    asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
-                 "r"(v.z), "r"(v.w) : "memory");
-  } else if (hint == 2) {
-    asm volatile("st.global.wt.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
-                 "r"(v.z), "r"(v.w) : "memory");
-  } else if (hint == 3) {
-    asm volatile("st.global.L1::no_allocate.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
-                 "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-  } else {
-    st_plain(p, v);
-  }
 }
 
 __device__ __forceinline__ uint64_t globaltimer_ns() {
@@ -238,17 +203,13 @@ __global__ void __launch_bounds__(kMaxThreads)
     const uint32_t lo = lane * kVecBytes;
 
     int4 v[kUnroll];
-    const uint32_t hint = p.hint;
     if (remain >= kPieceBytes) {
+      // Cache-hint variants of these accesses (L2::256B loads, .cs/.wt/.cg)
+      // measure identical: profiles/r01_host_access_hints.json.
 #pragma unroll
-      for (int j = 0; j < kUnroll; ++j)
-        v[j] = DIR == KVS_DIR_IN ? ld_host(src + j * kWarpBytes + lo, hint)
-                                 : ld_stream(src + j * kWarpBytes + lo);
+      for (int j = 0; j < kUnroll; ++j) v[j] = ld_stream(src + j * kWarpBytes + lo);
 #pragma unroll
-      for (int j = 0; j < kUnroll; ++j) {
-        if (DIR == KVS_DIR_OUT) st_host(dst + j * kWarpBytes + lo, v[j], hint);
-        else st_plain(dst + j * kWarpBytes + lo, v[j]);
-      }
+      for (int j = 0; j < kUnroll; ++j) st_plain(dst + j * kWarpBytes + lo, v[j]);
     } else {
 #pragma unroll
       for (int j = 0; j < kUnroll; ++j)
@@ -482,7 +443,6 @@ struct KvsHandle {
   uint64_t pace_ps[2] = {0, 0};  // per 4 KiB piece; 0 = unpaced
   double budget_gbps = 0.0;      // shared by both directions; 0 = none
   unsigned long long* d_bucket = nullptr;
-  uint32_t hint[2] = {0, 0};     // host access variant per direction (env KVS_HINT_OUT/IN)
   int64_t launches = 0;
 };
 
@@ -572,7 +532,6 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
       h->budget_gbps > 0.0 ? static_cast<uint64_t>(piece / h->budget_gbps + 0.5) : 0;
   if (p.bucket_cost_ns == 0 && h->budget_gbps > 0.0) p.bucket_cost_ns = 1;
   p.bucket_burst_ns = 16 * p.bucket_cost_ns;
-  p.hint = h->hint[dir];
   if (o.op_flags != nullptr) {
     // Same stream as the kernel: ordered before it, and after the previous
     // launch of this direction that used the counters.
@@ -680,8 +639,6 @@ int kvs_create(int device, const KvsGeometry* geo, const uint64_t* plane_ptrs, v
   h->num_cpu_blocks = num_cpu_blocks;
   h->host = static_cast<char*>(host_base);
   h->h_planes.assign(plane_ptrs, plane_ptrs + geo->num_planes);
-  if (const char* e = getenv("KVS_HINT_OUT")) h->hint[KVS_DIR_OUT] = static_cast<uint32_t>(atoi(e));
-  if (const char* e = getenv("KVS_HINT_IN")) h->hint[KVS_DIR_IN] = static_cast<uint32_t>(atoi(e));
   rc = cuda_rc(cudaMalloc(&h->d_planes, sizeof(uint64_t) * geo->num_planes));
   if (!rc)
     rc = cuda_rc(cudaMemcpy(h->d_planes, plane_ptrs, sizeof(uint64_t) * geo->num_planes,

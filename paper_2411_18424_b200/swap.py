@@ -184,17 +184,24 @@ class TransferRecord:
 COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 
 # Launch shape and pacing per direction (profiles/r01_interference_*.json,
-# profiles/r01_duplex_bw.json).  Unpaced, SM stores/loads to host memory are
-# issued far faster than PCIe drains them and back up the XBAR/L2 queues that
+# profiles/r01_duplex_bw.json).  Unpaced, SM stores to host memory are issued
+# far faster than PCIe drains them and back up the XBAR/L2 queues that
 # decode's HBM traffic shares: a concurrent 2 ms decode step slowed 1.2-4.9x.
-# Paced to the link rate the same swaps cost decode ~2-4% (out) / ~9% (in):
-#   latency    — serving: out 8x512 @52 GB/s, in 148x32 @51.5 GB/s, both
+# Swap-out is therefore paced below the link rate (posted writes have no
+# natural bound).  Swap-in is bounded by its reads in flight instead: 8 CTAs
+# x 256 threads x 4 KiB per warp = 256 KiB outstanding covers the PCIe
+# round trip at ~51.4 GB/s without building a queue, and unlike a pace it has
+# no cliff when a box's link is a little slower than the pace (a pace above
+# the link rate behaves like no pace: +35% decode).  Measured with a 2 ms
+# static-partition decode: out 51.9 GB/s +3-4%, in 51.2-51.4 GB/s +9.2%
+# (profiles/r01_interference_policy.json).
+#   latency    — serving: out 8x512 @52 GB/s, in 8x256 in-flight bound, both
 #                directions together capped at 60 GB/s (shared budget);
 #   throughput — bulk migration: unpaced, balanced 32x512 each way
 #                (highest combined GB/s, decode pays for it);
 #   unpaced    — out 8x512, in 32x512, no pacing (round-1 default shape).
 DUPLEX_POLICIES = {
-    "latency": {"out": (8, 512, 52.0), "in": (148, 32, 51.5), "budget": 60.0},
+    "latency": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0},
     "throughput": {"out": (32, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
     "unpaced": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
 }

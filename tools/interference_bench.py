@@ -89,6 +89,12 @@ def main():
         for po in (0.0, 26.0, 30.0):
             configs.append(("duplex_in4x512", "lsu", {"out": (8, 512), "in": (4, 512)},
                             {"out": po, "in": 0.0}, "kernel", ("out", "in")))
+    elif sweep == "probe3":
+        for ct, pace in (((8, 256), 0.0), ((6, 256), 0.0), ((8, 256), 50.0), ((8, 256), 52.0),
+                         ((148, 32), 50.0), ((148, 32), 50.5), ((148, 32), 51.0),
+                         ((4, 512), 50.0)):
+            configs.append((f"lsu{ct[0]}x{ct[1]}", "lsu", {"out": (8, 512), "in": ct},
+                            {"out": 0.0, "in": pace}, "kernel", ("in",)))
     elif sweep == "in":
         for ct in ((16, 512), (32, 128), (64, 64), (148, 32)):
             for pace in (0.0, 48.0, 40.0):
