@@ -411,3 +411,36 @@ def test_pacing_and_shared_budget(cuda_ok, path):
     assert total < 33.0, total  # shared 30 GB/s budget (+ idle burst credit)
     dp.set_budget(0.0)
     host.close()
+
+
+@pytest.mark.parametrize("model,tp", [("qwen2.5-32b", 2), ("qwen2.5-32b", 4),
+                                      ("qwen2.5-32b", 8), ("llama3-70b", 8)])
+def test_tp_shard_shapes_vs_oracle(cuda_ok, model, tp):
+    """BASELINE configs 4-5: per-rank KV shards (32 / 16 / 8 KiB chunks, 64-80
+    planes), C5-like long runs; swap-out byte-exact vs the oracle, then
+    swap-in to a new table == the oracle's restatement of the same ops."""
+    torch = cuda_ok
+    from paper_2411_18424_b200.geometry import PRESETS
+
+    geo = PRESETS[model].with_tp(tp)
+    G = C = 768
+    cache, host, dp = _mk(torch, geo, G, C)
+    rng = np.random.default_rng(tp)
+    pattern = orc.kv_pattern(tp, geo.num_planes, G, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    ops = orc.random_runs(rng, 600, 145, G, C)  # C5: mean 145 blocks per op
+    host.array[:] = 0
+    dp.swap("out", ops)
+    torch.cuda.synchronize()
+    want = np.zeros((C, geo.block_bytes), dtype=np.uint8)
+    orc.apply_plan("out", pattern, want, ops)
+    np.testing.assert_array_equal(host.array, want)
+    cache.planes.fill_(0xA5)
+    torch.cuda.synchronize()
+    in_ops = orc.random_runs(rng, 600, 37, G, C)
+    dp.swap("in", in_ops)
+    torch.cuda.synchronize()
+    want_planes = np.full_like(pattern, 0xA5)
+    orc.apply_plan("in", want_planes, want, in_ops)
+    assert np.array_equal(cache.planes.cpu().numpy(), want_planes)
+    host.close()
