@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace-convs", type=int, default=64)
     ap.add_argument("--no-trace", action="store_true")
+    ap.add_argument("--sm-partition", type=int, default=0,
+                    help="swap kernels on their own N-SM green context, decode on the rest")
     return ap.parse_args()
 
 
@@ -316,6 +318,10 @@ def run_ours(args, geo):
 
     # ---- serving configuration: paced swaps under a concurrent decode load ----
     serving = serving_interference(dp, dev, s) if rank == 0 else None
+    if rank == 0 and args.sm_partition:
+        serving = {"shared_sms": serving,
+                   f"swap_on_{args.sm_partition}_sms": serving_interference(
+                       dp, dev, s, args.sm_partition)}
 
     # ---- live multi-turn preemption trace: P99 TTFT / TBT (metric part 2) ----
     trace = None
@@ -452,7 +458,12 @@ def run_trace(args, geo, dev):
         from paper_2411_18424_b200.live import RankAgreement
         geo = geo.with_tp(world)
         agreement = RankAgreement(device=dev)
-    decode = DecodeEmulator(dev, weight_bytes=16 << 30)
+    stream, ctas, sms = None, 0, None
+    if args.sm_partition:
+        from paper_2411_18424_b200.swap import partition_streams
+        _, stream, sms = partition_streams(dev, args.sm_partition)
+        ctas = 2 * sms[1]
+    decode = DecodeEmulator(dev, weight_bytes=16 << 30, ctas=ctas, stream=stream)
     doc = {"block": {"bytes_per_block": geo.block_bytes}, "gpu_pool": {"total_blocks": 512},
            "cpu_pool": {"total_blocks": 4096},
            "workload": {"num_conversations": args.trace_convs, "arrival_rate_per_s": 4.0,
@@ -462,13 +473,13 @@ def run_trace(args, geo, dev):
                        f"{geo.block_bytes / 2**20:g} MiB GPU blocks per rank (TP{world}), "
                        f"Markov f=0.04, decode = {decode.bytes_per_us / 1e3:.0f} GB/s weight "
                        f"streaming per rank",
-           "tp": world, "runs": {}}
+           "tp": world, "sm_partition": sms, "runs": {}}
     for name, mode, impl in (("fastswitch", "full", "kernel"),
                              ("vllm_like", "baseline", "ce_per_block")):
         cfg, wl, _ = mconfig.build({**doc, "ablation": mode})
         cfg = dataclasses.replace(cfg, transfer=b200_transfer_params())
         rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, device=dev,
-                     copy_impl=impl, timing=True)
+                     copy_impl=impl, timing=True, sm_partition=args.sm_partition)
         eng = LiveEngine(cfg, generate(wl), rt, decode, agreement=agreement)
         eng.turn_trace = []
         rep = eng.run()
@@ -491,7 +502,7 @@ def run_trace(args, geo, dev):
     return out
 
 
-def serving_interference(dp, dev, s):
+def serving_interference(dp, dev, s, sm_partition: int = 0):
     """Swap-induced decode stall, measured: 2 ms HBM-streaming decode steps on a
     high-priority stream while a 2 GiB swap runs, per direction, with the
     serving ("latency") policy: paced kernels + shared budget (swap.py)."""
@@ -503,9 +514,15 @@ def serving_interference(dp, dev, s):
     from paper_2411_18424_b200.live import DecodeEmulator
     from paper_2411_18424_b200.swap import DUPLEX_POLICIES
 
-    dec = DecodeEmulator(dev, weight_bytes=16 << 30)
-    comp = torch.cuda.Stream(device=dev, priority=-1)
-    s2 = torch.cuda.Stream(device=dev)
+    if sm_partition:
+        from paper_2411_18424_b200.swap import partition_streams
+        (s, s2), comp, sms = partition_streams(dev, sm_partition)
+        dec = DecodeEmulator(dev, weight_bytes=16 << 30, ctas=2 * sms[1], stream=comp)
+    else:
+        sms = None
+        dec = DecodeEmulator(dev, weight_bytes=16 << 30)
+        comp = torch.cuda.Stream(device=dev, priority=-1)
+        s2 = torch.cuda.Stream(device=dev)
     rng = np.random.default_rng(5)
     n = 1024
     ops = random_runs(rng, n, 16, POOL_BLOCKS // 2, HOST_POOL_BLOCKS // 2).astype(np.int32)
@@ -533,7 +550,8 @@ def serving_interference(dp, dev, s):
         dp.set_launch(d, c, t)
         dp.set_pace(d, pace)
     dp.set_budget(pol["budget"])
-    out = {"policy": "latency", "decode_step_solo_ms": round(solo, 3), "runs": {}}
+    out = {"policy": "latency", "sm_partition": sms, "decode_step_solo_ms": round(solo, 3),
+           "runs": {}}
     for name, dirs in (("out", ("out",)), ("in", ("in",)), ("duplex", ("out", "in"))):
         torch.cuda.synchronize()
         t = {}

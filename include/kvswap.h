@@ -159,6 +159,19 @@ int64_t kvs_launch_count(const KvsHandle* h);
 int kvs_memcpy_baseline(KvsHandle* h, int dir, int mode, const int32_t* ops,
                         int32_t n_ops, uint64_t stream);
 
+/* Spatial SM partition for the swap kernels (green contexts): the swap side
+ * gets a group of >= swap_sms SMs (rounded up to the architecture's
+ * granularity, 8 on sm_90+) and the rest of the device's SMs form the
+ * compute side; n_swap_streams (1..16) non-blocking streams on the swap side
+ * and one on the compute side (CUstream values as uint64_t, usable with
+ * kvs_swap* / any kernel launch), sms_out[0..1] = SMs per side.  Kernels in one side never run on the other's SMs, so SM-issued
+ * host reads stop sharing SMs with decode CTAs.  Replaces: the reference's
+ * dispatch yield bound (swap.py:256-268) as a spatial rather than temporal
+ * bound.  Lives until process exit. */
+int kvs_sm_partition(int device, int swap_sms, int n_swap_streams, int swap_priority,
+                     int rest_priority, uint64_t* swap_streams, uint64_t* rest_stream,
+                     int* sms_out);
+
 /* Pinned, device-mapped host pool (CpuStore's backing bytes,
  * cpu_store.py:126-141).  numa_node < 0: no binding.  *dev receives the
  * device-usable address (== *host under UVA). */

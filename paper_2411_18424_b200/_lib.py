@@ -55,6 +55,7 @@ EXPORTED_SYMBOLS = (
     "kvs_memcpy_baseline",
     "kvs_host_alloc",
     "kvs_host_free",
+    "kvs_sm_partition",
     "kvs_stream_read",  # include/kvswap_workload.h
     "kvs_kv_tokens",  # include/kvswap_workload.h
 )
@@ -130,6 +131,10 @@ def _declare(lib: ctypes.CDLL) -> None:
     ]
     lib.kvs_host_free.restype = c.c_int
     lib.kvs_host_free.argtypes = [c.c_void_p]
+    lib.kvs_sm_partition.restype = c.c_int
+    lib.kvs_sm_partition.argtypes = [c.c_int, c.c_int, c.c_int, c.c_int, c.c_int,
+                                     c.POINTER(c.c_uint64), c.POINTER(c.c_uint64),
+                                     c.POINTER(c.c_int)]
     lib.kvs_stream_read.restype = c.c_int
     lib.kvs_stream_read.argtypes = [c.c_int, c.c_uint64, c.c_void_p, c.c_size_t, c.c_size_t,
                                     c.c_int, c.c_void_p]

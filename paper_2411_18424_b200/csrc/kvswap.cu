@@ -1144,3 +1144,79 @@ extern "C" int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_
   }
   return KVS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// SM partitioning with green contexts (include/kvswap.h, kvs_sm_partition).
+// The swap kernels get a small SM group of their own and decode the rest, so
+// SM-issued host reads never share an SM with a decode CTA.
+// ---------------------------------------------------------------------------
+namespace {
+
+using DeviceGetFn = CUresult (*)(CUdevice*, int);
+using DevResFn = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+using SplitFn = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*,
+                             unsigned, unsigned);
+using GenDescFn = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
+using GreenCreateFn = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+using GreenStreamFn = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+
+struct Partition {
+  CUgreenCtx ctx[2];
+  std::vector<CUstream> streams;
+};
+std::mutex g_part_mu;
+std::vector<Partition> g_parts;
+
+int drv_rc(CUresult r) { return r == CUDA_SUCCESS ? KVS_OK : KVS_ERR_UNSUPPORTED; }
+
+}  // namespace
+
+extern "C" int kvs_sm_partition(int device, int swap_sms, int n_swap_streams, int swap_priority,
+                                int rest_priority, uint64_t* swap_streams, uint64_t* rest_stream,
+                                int* sms_out) {
+  if (device < 0 || swap_sms < 1 || n_swap_streams < 1 || n_swap_streams > 16 ||
+      swap_streams == nullptr || rest_stream == nullptr || sms_out == nullptr)
+    return KVS_ERR_INVALID;
+  static auto dev_get = driver_fn<DeviceGetFn>("cuDeviceGet");
+  static auto dev_res = driver_fn<DevResFn>("cuDeviceGetDevResource");
+  static auto split = driver_fn<SplitFn>("cuDevSmResourceSplitByCount");
+  static auto gen = driver_fn<GenDescFn>("cuDevResourceGenerateDesc");
+  static auto create = driver_fn<GreenCreateFn>("cuGreenCtxCreate");
+  static auto gstream = driver_fn<GreenStreamFn>("cuGreenCtxStreamCreate");
+  if (!dev_get || !dev_res || !split || !gen || !create || !gstream) return KVS_ERR_UNSUPPORTED;
+  int rc = cuda_rc(cudaSetDevice(device));
+  if (rc) return rc;
+  rc = cuda_rc(cudaFree(nullptr));  // the primary context exists
+  if (rc) return rc;
+  CUdevice dev;
+  if ((rc = drv_rc(dev_get(&dev, device)))) return rc;
+  CUdevResource all{}, groups[1]{}, rest{};
+  if ((rc = drv_rc(dev_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM)))) return rc;
+  unsigned n = 1;
+  if ((rc = drv_rc(split(groups, &n, &all, &rest, 0, static_cast<unsigned>(swap_sms))))) return rc;
+  if (n != 1 || rest.sm.smCount == 0) return KVS_ERR_INVALID;
+  Partition part{};
+  CUdevResource* res[2] = {&groups[0], &rest};
+  const int prio[2] = {swap_priority, rest_priority};
+  for (int i = 0; i < 2; ++i) {
+    CUdevResourceDesc desc;
+    if ((rc = drv_rc(gen(&desc, res[i], 1)))) return rc;
+    if ((rc = drv_rc(create(&part.ctx[i], desc, dev, CU_GREEN_CTX_DEFAULT_STREAM)))) return rc;
+    const int n = i == 0 ? n_swap_streams : 1;
+    for (int k = 0; k < n; ++k) {
+      CUstream st;
+      if ((rc = drv_rc(gstream(&st, part.ctx[i], CU_STREAM_NON_BLOCKING, prio[i])))) return rc;
+      part.streams.push_back(st);
+    }
+  }
+  for (int k = 0; k < n_swap_streams; ++k)
+    swap_streams[k] = reinterpret_cast<uint64_t>(part.streams[k]);
+  *rest_stream = reinterpret_cast<uint64_t>(part.streams.back());
+  {
+    std::lock_guard<std::mutex> lock(g_part_mu);
+    g_parts.push_back(part);
+  }
+  sms_out[0] = static_cast<int>(groups[0].sm.smCount);
+  sms_out[1] = static_cast<int>(rest.sm.smCount);
+  return KVS_OK;
+}

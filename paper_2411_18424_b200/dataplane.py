@@ -78,6 +78,24 @@ def gpu_numa_node(device: Union[int, str, torch.device, None]) -> int:
         return -1
 
 
+def sm_partition(device=None, swap_sms: int = 8, swap_streams: int = 2,
+                 swap_priority: int = 0, compute_priority: int = -1):
+    """Green-context SM partition (kvs_sm_partition): returns
+    (swap streams, compute stream, (swap SMs, compute SMs)); the streams are
+    torch.cuda.ExternalStream views of the driver streams."""
+    lib = _lib.load()
+    idx = torch.device(device if device is not None else "cuda").index
+    idx = idx if idx is not None else torch.cuda.current_device()
+    swaps = (ctypes.c_uint64 * swap_streams)()
+    rest = ctypes.c_uint64()
+    sms = (ctypes.c_int * 2)()
+    _lib.check(lib.kvs_sm_partition(idx, swap_sms, swap_streams, swap_priority, compute_priority,
+                                    swaps, ctypes.byref(rest), sms), "kvs_sm_partition")
+    dev = torch.device("cuda", idx)
+    return ([torch.cuda.ExternalStream(int(h), device=dev) for h in swaps],
+            torch.cuda.ExternalStream(int(rest.value), device=dev), (sms[0], sms[1]))
+
+
 class HostKVPool:
     """Pinned, device-mapped host swap space: [num_blocks, block_bytes] bytes.
 

@@ -53,7 +53,10 @@ def b200_transfer_params(gbs: float = 51.0) -> TransferParams:
 class DecodeEmulator:
     """Weight-streaming decode stand-in (include/kvswap_workload.h)."""
 
-    def __init__(self, device, weight_bytes: int = 16 << 30, ctas: int = 0) -> None:
+    def __init__(self, device, weight_bytes: int = 16 << 30, ctas: int = 0,
+                 stream=None) -> None:
+        """`stream`: where decode will run (calibrated there, e.g. the compute
+        side of an SM partition); `ctas` 0 = 2 x the device's SMs."""
         self.lib = _lib.load()
         self.device = torch.device(device)
         self.index = self.device.index if self.device.index is not None else 0
@@ -62,6 +65,7 @@ class DecodeEmulator:
         self.sink = torch.zeros(4, dtype=torch.int32, device=self.device)
         torch.cuda.synchronize(self.device)  # calibrate on an idle GPU
         self.ctas = ctas
+        self.stream = stream
         self.bytes_per_us = self.calibrate()
 
     def launch(self, stream, nbytes: int) -> None:
@@ -77,7 +81,7 @@ class DecodeEmulator:
         return nbytes
 
     def calibrate(self, nbytes: int = 8 << 30) -> float:
-        s = torch.cuda.Stream(device=self.device)
+        s = self.stream if self.stream is not None else torch.cuda.Stream(device=self.device)
         self.launch(s, nbytes)
         s.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

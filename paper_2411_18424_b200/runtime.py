@@ -62,7 +62,7 @@ class Runtime:
     def __init__(self, geometry: KVGeometry, gpu_blocks: int, cpu_blocks: int,
                  device="cuda:0", copy_impl: str = "kernel", write_kv: bool = True,
                  verify: bool = False, timing: bool = False,
-                 duplex_policy: str = "latency") -> None:
+                 duplex_policy: str = "latency", sm_partition: int = 0) -> None:
         if geometry.split_kv:
             raise ValueError("runtime token writes assume fused K/V planes")
         self.geometry = geometry
@@ -70,7 +70,7 @@ class Runtime:
         self.host = HostKVPool(cpu_blocks, geometry.block_bytes, numa_node=None, device=device)
         self.dataplane = SwapDataPlane(self.cache, self.host)
         self.executor = StreamExecutor(self.dataplane, copy_impl=copy_impl, timing=timing,
-                                       duplex_policy=duplex_policy)
+                                       duplex_policy=duplex_policy, sm_partition=sm_partition)
         self.write_kv = write_kv
         self.verify = verify
         self.verified = 0

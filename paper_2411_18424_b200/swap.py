@@ -212,6 +212,21 @@ MAX_OP_WAITS = 8
 FLAG_RING = 1 << 20
 
 
+_PARTITIONS: dict = {}
+
+
+def partition_streams(device, swap_sms: int):
+    """One green-context partition per (device, swap_sms) per process (they
+    live until exit): ((out stream, in stream), compute stream, (swap SMs,
+    compute SMs))."""
+    from .dataplane import sm_partition
+
+    key = (str(device), swap_sms)
+    if key not in _PARTITIONS:
+        _PARTITIONS[key] = sm_partition(device, swap_sms=swap_sms, swap_streams=2)
+    return _PARTITIONS[key]
+
+
 class StreamExecutor:
     """Real streams + event hazards around one SwapDataPlane (one rank).
 
@@ -223,7 +238,7 @@ class StreamExecutor:
 
     def __init__(self, dataplane, compute_stream=None, copy_impl: str = "kernel",
                  timing: bool = False, duplex_policy: str = "latency",
-                 op_granular: bool = True) -> None:
+                 op_granular: bool = True, sm_partition: int = 0) -> None:
         import torch
 
         if copy_impl not in COPY_IMPLS:
@@ -231,10 +246,20 @@ class StreamExecutor:
         self.torch = torch
         self.dp = dataplane
         dev = dataplane.cache.device
-        self.streams = {
-            "out": torch.cuda.Stream(device=dev, priority=0),
-            "in": torch.cuda.Stream(device=dev, priority=0),
-        }
+        self.sm_split = None
+        if sm_partition:
+            # Swap streams on their own SM group, compute on the rest (green
+            # contexts, kvs_sm_partition): SM-issued host traffic never shares
+            # an SM with a decode CTA.
+            (s_out, s_in), part_compute, self.sm_split = partition_streams(dev, sm_partition)
+            self.streams = {"out": s_out, "in": s_in}
+            if compute_stream is None:
+                compute_stream = part_compute
+        else:
+            self.streams = {
+                "out": torch.cuda.Stream(device=dev, priority=0),
+                "in": torch.cuda.Stream(device=dev, priority=0),
+            }
         self.compute = compute_stream if compute_stream is not None else \
             torch.cuda.Stream(device=dev, priority=-1)
         self.copy_impl = copy_impl

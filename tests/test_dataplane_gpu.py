@@ -444,3 +444,37 @@ def test_tp_shard_shapes_vs_oracle(cuda_ok, model, tp):
     orc.apply_plan("in", want_planes, want, in_ops)
     assert np.array_equal(cache.planes.cpu().numpy(), want_planes)
     host.close()
+
+
+def test_sm_partition_streams_move_exact_bytes(cuda_ok):
+    """kvs_sm_partition (green contexts): swap kernels launched on the swap
+    side's streams, a torch kernel on the compute side; bytes exact."""
+    torch = cuda_ok
+    from paper_2411_18424_b200.swap import partition_streams
+
+    (s_out, s_in), comp, sms = partition_streams(torch.device("cuda:0"), 8)
+    props = torch.cuda.get_device_properties(0)
+    assert sms[0] >= 8 and sms[0] + sms[1] == props.multi_processor_count
+    geo = _small_geometry(1024, 4)
+    G = C = 256
+    cache, host, dp = _mk(torch, geo, G, C)
+    pattern = orc.kv_pattern(21, geo.num_planes, G, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(21)
+    ops = orc.random_runs(rng, 120, 8, G, C)
+    host.array[:] = 0
+    dp.swap("out", ops, stream=s_out)
+    s_out.synchronize()
+    want = np.zeros((C, geo.block_bytes), dtype=np.uint8)
+    orc.apply_plan("out", pattern, want, ops)
+    np.testing.assert_array_equal(host.array, want)
+    with torch.cuda.stream(comp):
+        cache.planes.fill_(0x3C)  # compute side: a torch kernel on the other SM group
+    comp.synchronize()
+    dp.swap("in", ops, stream=s_in)
+    s_in.synchronize()
+    want_planes = np.full_like(pattern, 0x3C)
+    orc.apply_plan("in", want_planes, want, ops)
+    assert np.array_equal(cache.planes.cpu().numpy(), want_planes)
+    host.close()

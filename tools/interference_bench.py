@@ -46,8 +46,15 @@ def main():
     cache.planes.view(torch.int32).random_()
     dec = DecodeEmulator("cuda:0", weight_bytes=16 << 30,
                          ctas=int(os.environ.get("DECODE_CTAS", "0")))
-    comp = torch.cuda.Stream(priority=-1)
-    s_out, s_in = torch.cuda.Stream(), torch.cuda.Stream()
+    green = int(os.environ.get("GREEN", "0"))
+    if green:
+        # swap kernels on their own SM group (green contexts), decode on the rest
+        from paper_2411_18424_b200.dataplane import sm_partition
+        (s_out, s_in), comp, sms = sm_partition("cuda:0", swap_sms=green, swap_streams=2)
+    else:
+        comp = torch.cuda.Stream(priority=-1)
+        s_out, s_in = torch.cuda.Stream(), torch.cuda.Stream()
+        sms = None
     rng = np.random.default_rng(0)
     half = POOL // 2
     ops_out = orc.random_runs(rng, half, 16, half, half).astype(np.int32)
@@ -61,7 +68,8 @@ def main():
     evs = decode_steps(dec, comp, 40)
     torch.cuda.synchronize()
     solo = statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(40))
-    results = {"decode_step_solo_ms": round(solo, 4), "decode_ctas": dec.ctas, "runs": []}
+    results = {"decode_step_solo_ms": round(solo, 4), "decode_ctas": dec.ctas,
+               "sm_partition": sms, "runs": []}
     print(json.dumps(results), flush=True)
 
     # (label, path, {dir: (ctas, threads)}, {dir: pace GB/s}, impl, dirs)
@@ -95,6 +103,17 @@ def main():
                          ((4, 512), 50.0)):
             configs.append((f"lsu{ct[0]}x{ct[1]}", "lsu", {"out": (8, 512), "in": ct},
                             {"out": 0.0, "in": pace}, "kernel", ("in",)))
+    elif sweep == "probe4":
+        for ct, pace in (((8, 256), 0.0), ((148, 32), 50.0), ((32, 512), 0.0), ((8, 512), 0.0)):
+            configs.append((f"lsu{ct[0]}x{ct[1]}", "lsu", {"out": (8, 512), "in": ct},
+                            {"out": 0.0, "in": pace}, "kernel", ("in",)))
+        for ct, pace in (((8, 512), 52.0), ((8, 512), 0.0), ((32, 512), 0.0)):
+            configs.append((f"lsu{ct[0]}x{ct[1]}", "lsu", {"out": ct, "in": (8, 256)},
+                            {"out": pace, "in": 0.0}, "kernel", ("out",)))
+        configs.append(("duplex", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 0.0, "in": 0.0}, "kernel", ("out", "in")))
+        configs.append(("duplex_paced", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 52.0, "in": 0.0}, "kernel", ("out", "in")))
     elif sweep == "in":
         for ct in ((16, 512), (32, 128), (64, 64), (148, 32)):
             for pace in (0.0, 48.0, 40.0):

@@ -36,7 +36,8 @@ def run_one(args, mode, impl, decode, geo):
     cfg, wl, _ = mconfig.build(doc)
     cfg = type(cfg)(**{**cfg.__dict__, "transfer": b200_transfer_params(args.pcie_gbs)})
     rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, copy_impl=impl,
-                 verify=args.verify, timing=True, duplex_policy=args.policy)
+                 verify=args.verify, timing=True, duplex_policy=args.policy,
+                 sm_partition=args.sm_partition)
     eng = LiveEngine(cfg, generate(wl), rt, decode)
     eng.turn_trace = []
     t0 = time.perf_counter()
@@ -88,10 +89,18 @@ def main():
     ap.add_argument("--weights-gib", type=int, default=16)
     ap.add_argument("--verify", action="store_true")
     ap.add_argument("--policy", default="latency")
+    ap.add_argument("--sm-partition", type=int, default=0,
+                    help="swap kernels on their own N-SM green context, decode on the rest")
     ap.add_argument("--out", default="gpurun_out/live_trace.json")
     args = ap.parse_args()
     geo = PRESETS[args.model]
-    decode = DecodeEmulator("cuda:0", weight_bytes=args.weights_gib << 30)
+    stream, ctas = None, 0
+    if args.sm_partition:
+        from paper_2411_18424_b200.swap import partition_streams
+        _, stream, sms = partition_streams(torch.device("cuda:0"), args.sm_partition)
+        ctas = 2 * sms[1]
+    decode = DecodeEmulator("cuda:0", weight_bytes=args.weights_gib << 30, ctas=ctas,
+                            stream=stream)
     results = {"decode_calibrated_gbs": round(decode.bytes_per_us / 1e3, 1), "runs": []}
     for item in args.modes.split(","):
         mode, impl = item.split(":")
