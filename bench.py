@@ -58,8 +58,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace-convs", type=int, default=64)
     ap.add_argument("--no-trace", action="store_true")
-    ap.add_argument("--sm-partition", type=int, default=0,
-                    help="swap kernels on their own N-SM green context, decode on the rest")
+    ap.add_argument("--sm-partition", type=int, default=8,
+                    help="serving + trace: swap kernels on their own N-SM green context, "
+                         "decode on the rest (0 = share all SMs)")
     return ap.parse_args()
 
 
