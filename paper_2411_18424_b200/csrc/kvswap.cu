@@ -1159,6 +1159,8 @@ using SplitFn = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CU
 using GenDescFn = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
 using GreenCreateFn = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
 using GreenStreamFn = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+using GreenDestroyFn = CUresult (*)(CUgreenCtx);
+using StreamDestroyFn = CUresult (*)(CUstream);
 
 struct Partition {
   CUgreenCtx ctx[2];
@@ -1195,17 +1197,29 @@ extern "C" int kvs_sm_partition(int device, int swap_sms, int n_swap_streams, in
   unsigned n = 1;
   if ((rc = drv_rc(split(groups, &n, &all, &rest, 0, static_cast<unsigned>(swap_sms))))) return rc;
   if (n != 1 || rest.sm.smCount == 0) return KVS_ERR_INVALID;
+  static auto destroy_ctx = driver_fn<GreenDestroyFn>("cuGreenCtxDestroy");
+  static auto destroy_stream = driver_fn<StreamDestroyFn>("cuStreamDestroy");
   Partition part{};
+  auto unwind = [&](int err) {  // release what this call created
+    if (destroy_stream)
+      for (CUstream st : part.streams) destroy_stream(st);
+    if (destroy_ctx)
+      for (CUgreenCtx c : part.ctx)
+        if (c) destroy_ctx(c);
+    return err;
+  };
   CUdevResource* res[2] = {&groups[0], &rest};
   const int prio[2] = {swap_priority, rest_priority};
   for (int i = 0; i < 2; ++i) {
     CUdevResourceDesc desc;
-    if ((rc = drv_rc(gen(&desc, res[i], 1)))) return rc;
-    if ((rc = drv_rc(create(&part.ctx[i], desc, dev, CU_GREEN_CTX_DEFAULT_STREAM)))) return rc;
+    if ((rc = drv_rc(gen(&desc, res[i], 1)))) return unwind(rc);
+    if ((rc = drv_rc(create(&part.ctx[i], desc, dev, CU_GREEN_CTX_DEFAULT_STREAM))))
+      return unwind(rc);
     const int n = i == 0 ? n_swap_streams : 1;
     for (int k = 0; k < n; ++k) {
       CUstream st;
-      if ((rc = drv_rc(gstream(&st, part.ctx[i], CU_STREAM_NON_BLOCKING, prio[i])))) return rc;
+      if ((rc = drv_rc(gstream(&st, part.ctx[i], CU_STREAM_NON_BLOCKING, prio[i]))))
+        return unwind(rc);
       part.streams.push_back(st);
     }
   }

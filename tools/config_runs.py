@@ -8,6 +8,8 @@ the identical plan stream over its own PCIe link).
   c5  LLaMA-3-70B KV at 32K context, TP8 rank shard, high preemption — live
 
 python tools/config_runs.py c3 c4 c5   -> gpurun_out/config_runs.json
+(SM_PARTITION=8 by default: live runs put the swap kernels on their own 8-SM
+green context and decode on the rest; SM_PARTITION=0 shares all SMs.)
 """
 
 import dataclasses
@@ -30,6 +32,9 @@ from paper_2411_18424_b200.runtime import Runtime  # noqa: E402
 from paper_2411_18424_b200.workload import generate  # noqa: E402
 
 
+SM_PARTITION = int(os.environ.get("SM_PARTITION", "8"))
+
+
 def swap_rates(rt):
     ex = rt.executor
     out = {}
@@ -46,11 +51,13 @@ def live_run(geo, doc, impl="kernel", decode=None, verify=False):
     cfg, wl, _ = mconfig.build(doc)
     cfg = dataclasses.replace(cfg, transfer=b200_transfer_params())
     rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, copy_impl=impl,
-                 verify=verify, timing=True)
+                 verify=verify, timing=True, sm_partition=SM_PARTITION)
     eng = LiveEngine(cfg, generate(wl), rt, decode)
+    eng.turn_trace = []
     t0 = time.perf_counter()
     rep = eng.run()
     res = {"wall_s": round(time.perf_counter() - t0, 1), "latency": eng.latency_summary(),
+           "ttft_anatomy": eng.ttft_anatomy(),
            "swap": swap_rates(rt), "runtime": rt.stats(),
            "report": {k: rep.to_dict()[k] for k in (
                "total_tokens", "expected_tokens", "swap_out_blocks", "swap_in_blocks",
@@ -70,8 +77,9 @@ def c3(decode):
                                                decode=decode),
                         "vllm_like": live_run(LLAMA3_8B, {**doc, "ablation": "baseline"},
                                               impl="ce_per_block", decode=decode)}
-        print("c3", pattern, json.dumps({k: v["latency"] for k, v in out[pattern].items()}),
-              flush=True)
+        print("c3", pattern, json.dumps({k: {m: v["latency"][m] for m in (
+            "ttft_p50_ms", "ttft_p99_ms", "tbt_p99_ms", "tbt_p999_ms",
+            "swap_induced_decode_stall")} for k, v in out[pattern].items()}), flush=True)
     return out
 
 
@@ -122,7 +130,13 @@ def main():
     out = {}
     decode = None
     if "c3" in which or "c5" in which:
-        decode = DecodeEmulator("cuda:0", weight_bytes=16 << 30)
+        stream, ctas = None, 0
+        if SM_PARTITION:
+            from paper_2411_18424_b200.swap import partition_streams
+            _, stream, sms = partition_streams(torch.device("cuda:0"), SM_PARTITION)
+            ctas = 2 * sms[1]
+            out["sm_partition"] = sms
+        decode = DecodeEmulator("cuda:0", weight_bytes=16 << 30, ctas=ctas, stream=stream)
         out["decode_calibrated_gbs"] = round(decode.bytes_per_us / 1e3, 1)
     if "c4" in which:
         out["c4"] = c4()
