@@ -145,6 +145,24 @@ int kvs_swap_layered(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
 int kvs_swap_ops(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
                  uint64_t stream, uint32_t* op_flags, uint32_t* done_flag, uint32_t seq);
 
+/* Completion words one swap call may publish (all optional, seq-valued,
+ * system-scope release).  plane_flags != NULL selects plane-major order. */
+typedef struct KvsSignals {
+  uint32_t* op_flags;    /* n_ops words: TransferOp i landed (kvs_swap_ops)      */
+  uint32_t* plane_flags; /* num_planes words: plane p landed (kvs_swap_layered)  */
+  uint32_t* done_flag;   /* one word: the whole call landed (kvs_swap)           */
+  uint32_t seq;
+  uint32_t reserved;     /* must be 0 */
+} KvsSignals;
+
+/* One SwapPlan with any combination of the completion words above: a resumed
+ * request can join decode layer by layer (plane flags) while conflicting
+ * grants still wait per TransferOp (op flags).  Replaces, together:
+ * engine.py:376-384 (swap-in completion, iteration-wise in the reference,
+ * PAPER.md:103-105) and swap.py:236-252 (per-op conflict resolution). */
+int kvs_swap_signaled(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
+                      uint64_t stream, const KvsSignals* sig);
+
 /* Make `stream` wait until *flag >= value (cuStreamWaitValue32 GEQ).
  * Replaces: not_before / conflict dependencies (engine.py:712-719,
  * swap.py:236-252) as a device-side wait instead of a modeled timestamp. */

@@ -50,6 +50,7 @@ EXPORTED_SYMBOLS = (
     "kvs_swap",
     "kvs_swap_layered",
     "kvs_swap_ops",
+    "kvs_swap_signaled",
     "kvs_wait_flag",
     "kvs_launch_count",
     "kvs_memcpy_baseline",
@@ -69,6 +70,16 @@ class NativeLibraryError(RuntimeError):
 
 class KvSwapCudaError(RuntimeError):
     """A CUDA runtime/driver call inside libkvswap failed."""
+
+
+class KvsSignals(ctypes.Structure):
+    _fields_ = [
+        ("op_flags", ctypes.c_void_p),
+        ("plane_flags", ctypes.c_void_p),
+        ("done_flag", ctypes.c_void_p),
+        ("seq", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
+    ]
 
 
 class KvsGeometry(ctypes.Structure):
@@ -117,6 +128,9 @@ def _declare(lib: ctypes.CDLL) -> None:
         c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64, c.c_void_p, c.c_void_p,
         c.c_uint32,
     ]
+    lib.kvs_swap_signaled.restype = c.c_int
+    lib.kvs_swap_signaled.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64,
+                                      c.POINTER(KvsSignals)]
     lib.kvs_wait_flag.restype = c.c_int
     lib.kvs_wait_flag.argtypes = [c.c_uint64, c.c_void_p, c.c_uint32]
     lib.kvs_launch_count.restype = c.c_int64

@@ -771,6 +771,18 @@ int kvs_swap_layered(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, u
   return swap_impl(h, dir, ops, n_ops, stream, o);
 }
 
+int kvs_swap_signaled(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
+                      const KvsSignals* sig) {
+  if (sig == nullptr || sig->reserved != 0) return KVS_ERR_INVALID;
+  LaunchOpts o;
+  o.op_flags = sig->op_flags;
+  o.plane_flags = sig->plane_flags;
+  o.done_flag = sig->done_flag;
+  o.layered = sig->plane_flags != nullptr;
+  o.seq = sig->seq;
+  return swap_impl(h, dir, ops, n_ops, stream, o);
+}
+
 int kvs_swap_ops(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, uint64_t stream,
                  uint32_t* op_flags, uint32_t* done_flag, uint32_t seq) {
   if (op_flags == nullptr) return KVS_ERR_INVALID;

@@ -267,6 +267,21 @@ class SwapDataPlane:
         _lib.check(rc, f"kvs_swap_ops({direction})")
         return arr
 
+    def swap_signaled(self, direction: str, ops: OpsLike, seq: int,
+                      op_flags: Optional[int] = None, plane_flags: Optional[int] = None,
+                      done_flag: Optional[int] = None,
+                      stream: Optional[torch.cuda.Stream] = None) -> np.ndarray:
+        """One launch with any of: per-op flags, per-plane flags (plane-major
+        order), a whole-plan flag; each receives `seq` once its bytes landed."""
+        arr = ops_array(ops)
+        sig = _lib.KvsSignals(op_flags or None, plane_flags or None, done_flag or None,
+                              seq & 0xFFFFFFFF, 0)
+        rc = self.lib.kvs_swap_signaled(self.handle, _lib.DIRECTIONS[direction],
+                                        arr.ctypes.data_as(ctypes.c_void_p), arr.shape[0],
+                                        _stream_handle(stream), ctypes.byref(sig))
+        _lib.check(rc, f"kvs_swap_signaled({direction})")
+        return arr
+
     def baseline(self, direction: str, mode: int, ops: OpsLike,
                  stream: Optional[torch.cuda.Stream] = None) -> None:
         arr = ops_array(ops)

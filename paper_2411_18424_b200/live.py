@@ -167,13 +167,26 @@ class LiveEngine(Engine):
     with `agreement`, one TP rank of a group that decides in lockstep)."""
 
     def __init__(self, config: EngineConfig, conversations, runtime, decode: DecodeEmulator,
-                 time_scale: float = 1.0, agreement: Optional[RankAgreement] = None) -> None:
+                 time_scale: float = 1.0, agreement: Optional[RankAgreement] = None,
+                 layered: bool = False) -> None:
+        """layered: resumed requests join decode layer by layer (SURVEY §8f
+        rank 2).  A swap-in at the head of the swap-in stream whose modeled
+        completion falls inside this iteration joins the batch now, and so do
+        sync-mode swap-ins (swap.py:113-135); decode layer l waits only for
+        layer l of their KV (plane flags), instead of the reference's
+        iteration-wise completion (engine.py:376-384)."""
         if runtime is None:
             raise ValueError("live mode needs a Runtime (real data plane)")
         super().__init__(config, conversations, runtime=runtime)
         self.decode = decode
         self.time_scale = time_scale
         self.agreement = agreement
+        self.layered = layered and runtime.executor.layered_swap_in
+        if layered and not self.layered:
+            raise ValueError("layered admission needs Runtime(layered_swap_in=True) "
+                             "with the kernel copy path")
+        self._deferred: Optional[list] = None
+        self.layered_joins = 0
         self.live = LiveStats()
         # per computing iteration: (duration_us, cpu_us, wait_ms, kernel_ms,
         #                           synced, conflict_waits, n_prefill, n_decode)
@@ -218,6 +231,32 @@ class LiveEngine(Engine):
                 moved = True
         self.manager.in_flight = keep
         return moved
+
+    def _mark_running(self, req) -> bool:
+        if self._deferred is None:
+            return super()._mark_running(req)
+        # Joining layer by layer: running now, bytes checked once decode has
+        # waited for every layer (verification needs the whole KV).
+        from .engine import SWAPPING_IN
+        st = self.states.get(req)
+        if st is None or st.phase != SWAPPING_IN:
+            return False
+        st.phase = "running"
+        self.qs.move(req, "running")
+        self._mark_turn(req, 2)
+        self._deferred.append(req)
+        return True
+
+    def _join_layered(self, flights) -> list:
+        """Move `flights` (pending swap-ins) into the running set now; returns
+        their transfers, whose plane flags decode will wait on per layer."""
+        deps = []
+        self._deferred = self._deferred or []
+        for f in flights:
+            self.manager.in_flight.remove(f)
+            if self._mark_running(f.request):
+                deps.append(f.transfer)
+        return deps
 
     def _wait_any(self, budget_us: int) -> None:
         """Nothing to compute: block on the earliest pending transfer (or a tick)."""
@@ -329,13 +368,30 @@ class LiveEngine(Engine):
             decision = decide_mode(drain, biggest, est, self.cfg.sync_threshold_ratio,
                                    self.cfg.short_request_blocks,
                                    forced=None if self.mode.adaptive else "sync")
+            layer_deps: list = []
+            self._deferred = None
             if decision.mode == "sync" and pending:
                 self.sync_stall_count += 1
-                for f in pending:
-                    ex.wait_transfer(f.transfer)
-                    self.manager.in_flight.remove(f)
-                    self._mark_running(f.request)
+                if self.layered:
+                    layer_deps = self._join_layered(pending)
+                else:
+                    for f in pending:
+                        ex.wait_transfer(f.transfer)
+                        self.manager.in_flight.remove(f)
+                        self._mark_running(f.request)
                 progress = True
+            elif self.layered and pending:
+                # The head of the (FIFO) swap-in stream, and the ones right
+                # behind it, join now if modeled to land within this iteration.
+                ready = []
+                for f in pending:
+                    if elapsed(f.exec_done, self.clock) > est:
+                        break
+                    ready.append(f)
+                if ready:
+                    layer_deps = self._join_layered(ready)
+                    progress = True
+            self.layered_joins += len(layer_deps)
             if not self.mode.adaptive:
                 for f in list(self.manager.in_flight):
                     ex.wait_transfer(f.transfer)
@@ -352,16 +408,37 @@ class LiveEngine(Engine):
                 continue
             nominal_us = iteration_time(prefill_tokens, len(decoders), self.infer) * self.time_scale
             t_cpu = time.perf_counter()
-            self.runtime.compute(self, spans)
-            t_rt = time.perf_counter()
-            waits_seen = grant_waits + list(ex.last_barrier)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(compute)
-            swapping = any(not r.poll() for r in ex.pending)
-            nbytes = self.decode.launch_us(compute, nominal_us)
-            e1.record(compute)
+            if layer_deps:
+                # Decode layer by layer; layer l waits for layer l of every
+                # joining request's KV.  This iteration's KV writes follow the
+                # last layer, when every joining request's KV has landed.
+                swapping = True
+                e0.record(compute)
+                planes = self.runtime.geometry.num_planes
+                nbytes = 0
+                for layer in range(planes):
+                    for dep in layer_deps:
+                        ex.wait_plane(compute, dep, layer)
+                    nbytes += self.decode.launch_us(compute, nominal_us / planes)
+                e1.record(compute)
+                self.runtime.compute(self, spans, skip=layer_deps)
+                t_rt = time.perf_counter()
+                waits_seen = grant_waits + list(ex.last_barrier)
+            else:
+                self.runtime.compute(self, spans)
+                t_rt = time.perf_counter()
+                waits_seen = grant_waits + list(ex.last_barrier)
+                e0.record(compute)
+                swapping = any(not r.poll() for r in ex.pending)
+                nbytes = self.decode.launch_us(compute, nominal_us)
+                e1.record(compute)
             compute.synchronize()
+            if self._deferred:
+                for req in self._deferred:  # now every layer has landed
+                    self.runtime.swap_in_landed(self, req)
+            self._deferred = None
             end = self._end_clock()
             kernel_ms = e0.elapsed_time(e1)
             self._trace.append((end - start, int((t_cpu - t_iter) * 1e6), e_pre.elapsed_time(e0),
@@ -369,14 +446,15 @@ class LiveEngine(Engine):
                                 conf_now, len(prefillers),
                                 len(decoders), waits_seen[:6], int((t_rt - t_cpu) * 1e6)))
             nominal_ms = nbytes / self.decode.bytes_per_us / 1e3
-            self.live.decode_ms += kernel_ms
-            self.live.decode_nominal_ms += nominal_ms
-            if swapping:
-                self.live.busy_ms += kernel_ms
-                self.live.busy_nominal_ms += nominal_ms
-            else:
-                self.live.quiet_ms += kernel_ms
-                self.live.quiet_nominal_ms += nominal_ms
+            if not layer_deps:  # layered steps include data waits: not a decode-rate sample
+                self.live.decode_ms += kernel_ms
+                self.live.decode_nominal_ms += nominal_ms
+                if swapping:
+                    self.live.busy_ms += kernel_ms
+                    self.live.busy_nominal_ms += nominal_ms
+                else:
+                    self.live.quiet_ms += kernel_ms
+                    self.live.quiet_nominal_ms += nominal_ms
             self.live.iterations += 1
             duration = end - start
             emitted = self._emit_tokens(prefillers, decoders, end)
@@ -448,6 +526,7 @@ class LiveEngine(Engine):
                 self.live.busy_ms / max(1e-9, self.live.decode_ms), 4),
             "iterations": self.live.iterations,
             "idle_waits": self.live.idle_waits,
+            "layered_joins": self.layered_joins,
             "wall_s": round(self.live.wall_s, 2),
             "slow_iterations": self.spike_breakdown(),
             "tp_agreement": None if self.agreement is None else {

@@ -62,7 +62,8 @@ class Runtime:
     def __init__(self, geometry: KVGeometry, gpu_blocks: int, cpu_blocks: int,
                  device="cuda:0", copy_impl: str = "kernel", write_kv: bool = True,
                  verify: bool = False, timing: bool = False,
-                 duplex_policy: str = "latency", sm_partition: int = 0) -> None:
+                 duplex_policy: str = "latency", sm_partition: int = 0,
+                 layered_swap_in: bool = False) -> None:
         if geometry.split_kv:
             raise ValueError("runtime token writes assume fused K/V planes")
         self.geometry = geometry
@@ -70,7 +71,8 @@ class Runtime:
         self.host = HostKVPool(cpu_blocks, geometry.block_bytes, numa_node=None, device=device)
         self.dataplane = SwapDataPlane(self.cache, self.host)
         self.executor = StreamExecutor(self.dataplane, copy_impl=copy_impl, timing=timing,
-                                       duplex_policy=duplex_policy, sm_partition=sm_partition)
+                                       duplex_policy=duplex_policy, sm_partition=sm_partition,
+                                       layered_swap_in=layered_swap_in)
         self.write_kv = write_kv
         self.verify = verify
         self.verified = 0
@@ -107,13 +109,14 @@ class Runtime:
 
     # -- engine hooks ------------------------------------------------------------
 
-    def compute(self, engine, spans) -> None:
+    def compute(self, engine, spans, skip=()) -> None:
         """One iteration's compute on the compute stream: wait for conflicting
-        transfers, then write the KV of every produced token (one launch)."""
+        transfers (except `skip`, already waited for per layer), then write
+        the KV of every produced token (one launch)."""
         extents = []
         for req, _, _ in spans:
             extents.extend(engine._gpu_extents(req))
-        self.barrier_waits += self.executor.compute_barrier(extents)
+        self.barrier_waits += self.executor.compute_barrier(extents, skip=skip)
         if not self.write_kv:
             return
         segs = self.segments(engine, spans)

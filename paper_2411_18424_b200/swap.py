@@ -174,6 +174,8 @@ class TransferRecord:
     seq: int = 0
     submitted: float = 0.0  # host perf_counter at submit (diagnostics)
     deps: int = 0  # cross-stream waits this transfer was issued behind
+    plane_base: Optional[int] = None  # plane-flag slots [plane_base, + num_planes)
+    flag_span: int = 0  # flag slots this transfer owns (op + plane flags)
 
     def poll(self) -> bool:
         if not self.done and self.event.query():
@@ -238,7 +240,8 @@ class StreamExecutor:
 
     def __init__(self, dataplane, compute_stream=None, copy_impl: str = "kernel",
                  timing: bool = False, duplex_policy: str = "latency",
-                 op_granular: bool = True, sm_partition: int = 0) -> None:
+                 op_granular: bool = True, sm_partition: int = 0,
+                 layered_swap_in: bool = False) -> None:
         import torch
 
         if copy_impl not in COPY_IMPLS:
@@ -265,6 +268,10 @@ class StreamExecutor:
         self.copy_impl = copy_impl
         self.timing = timing
         self.op_granular = op_granular and copy_impl == "kernel"
+        # Swap-ins also publish one flag per plane (layer), moved plane-major,
+        # so compute can join a resumed request layer by layer (wait_plane).
+        self.layered_swap_in = layered_swap_in and self.op_granular
+        self.num_planes = dataplane.geometry.num_planes
         self.pending: list[TransferRecord] = []
         self.history: list[TransferRecord] = []
         self.bytes = {"out": 0, "in": 0}
@@ -299,7 +306,7 @@ class StreamExecutor:
             self._flag_head = 0
         base = self._flag_head
         for r in self.pending:  # never recycle slots a live transfer still signals
-            if r.flag_base is not None and r.flag_base < base + n and base < r.flag_base + len(r.gpu):
+            if r.flag_base is not None and r.flag_base < base + n and base < r.flag_base + r.flag_span:
                 r.event.synchronize()
         self._flag_head += n
         return base
@@ -344,15 +351,23 @@ class StreamExecutor:
         if self.timing:
             start = torch.cuda.Event(enable_timing=True)
             start.record(stream)
-        flag_base, seq = None, 0
+        flag_base, seq, plane_base, span = None, 0, None, 0
         if ops:
             if self.copy_impl == "kernel":
                 if self.op_granular:
-                    flag_base = self._claim_flags(len(ops))
+                    layered = self.layered_swap_in and direction == "in"
+                    span = len(ops) + (self.num_planes if layered else 0)
+                    flag_base = self._claim_flags(span)
                     self._seq += 1
                     seq = self._seq
-                    self.dp.swap_ops(direction, ops, self._flags_ptr + 4 * flag_base, seq,
-                                     stream=stream)
+                    op_ptr = self._flags_ptr + 4 * flag_base
+                    if layered:
+                        plane_base = flag_base + len(ops)
+                        self.dp.swap_signaled(direction, ops, seq, op_flags=op_ptr,
+                                              plane_flags=self._flags_ptr + 4 * plane_base,
+                                              stream=stream)
+                    else:
+                        self.dp.swap_ops(direction, ops, op_ptr, seq, stream=stream)
                 else:
                     self.dp.swap(direction, ops, stream=stream)
                 self.launches += 1
@@ -364,7 +379,7 @@ class StreamExecutor:
         blocks = sum(op.blocks for op in ops)
         rec = TransferRecord(direction, gpu, host, ev, blocks * self.block_bytes,
                              refresh_blocks * self.block_bytes, start, False, flag_base, seq,
-                             time.perf_counter(), deps)
+                             time.perf_counter(), deps, plane_base, span)
         self.bytes[direction] += rec.nbytes
         self.refresh_bytes += rec.refresh_bytes
         self.pending.append(rec)
@@ -372,15 +387,24 @@ class StreamExecutor:
             self.history.append(rec)
         return rec
 
-    def compute_barrier(self, extents: list[tuple[int, int]]) -> int:
+    def wait_plane(self, stream, rec: TransferRecord, plane: int) -> None:
+        """`stream` waits until plane `plane` of a layered transfer has landed."""
+        if rec.plane_base is None:
+            raise ValueError("transfer was not issued plane-major (layered_swap_in)")
+        self.dp.wait_flag(stream, self._flags_ptr + 4 * (rec.plane_base + plane), rec.seq)
+
+    def compute_barrier(self, extents: list[tuple[int, int]], skip=()) -> int:
         """Make the compute stream wait for transfers touching `extents`
-        (their blocking ops only, when op flags exist).
+        (their blocking ops only, when op flags exist); transfers in `skip`
+        are being waited for another way (per plane).
 
         Returns the number of transfers waited on (real conflicts)."""
         self._prune()
         n = 0
         self.last_barrier = []  # (direction, age_ms, ops waited, its deps, MiB)
         for r in self.pending:
+            if any(r is k for k in skip):
+                continue
             hits = _hit_ops(extents, r.gpu)
             if hits:
                 self._wait(self.compute, r, hits)

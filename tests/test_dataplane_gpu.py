@@ -478,3 +478,50 @@ def test_sm_partition_streams_move_exact_bytes(cuda_ok):
     orc.apply_plan("in", want_planes, want, ops)
     assert np.array_equal(cache.planes.cpu().numpy(), want_planes)
     host.close()
+
+
+@pytest.mark.parametrize("n_ops_big", [False, True])
+def test_signaled_swap_op_plane_and_done_flags(cuda_ok, n_ops_big):
+    """kvs_swap_signaled: per-op + per-plane + whole-plan words from one call
+    (plane-major order, > 2048 ops -> several launches); a consumer waiting on
+    plane l sees plane l complete; bytes exact vs the oracle."""
+    torch = cuda_ok
+    geo = _small_geometry(1028, 5)
+    G = C = 3000
+    cache, host, dp = _mk(torch, geo, G, C, ctas={"out": 4, "in": 4})
+    rng = np.random.default_rng(33)
+    pattern = orc.kv_pattern(8, geo.num_planes, G, geo.plane_chunk_bytes)
+    n = 2600 if n_ops_big else 400
+    gpu_tab = orc.random_block_table(rng, n, G)
+    cpu_tab = orc.random_block_table(rng, n, C)
+    ops = orc.table_to_ops(gpu_tab, cpu_tab)
+    assert (len(ops) > 2048) == n_ops_big
+    host_img = np.zeros((C, geo.block_bytes), np.uint8)
+    orc.apply_plan("out", pattern, host_img, ops)
+    host.array[:] = host_img
+    cache.planes.zero_()
+    torch.cuda.synchronize()
+    words = torch.zeros(len(ops) + geo.num_planes + 1, dtype=torch.int32, device="cuda:0")
+    base = words.data_ptr()
+    s_swap, s_use = torch.cuda.Stream(), torch.cuda.Stream()
+    dp.swap_signaled("in", ops, 5, op_flags=base, plane_flags=base + 4 * len(ops),
+                     done_flag=base + 4 * (len(ops) + geo.num_planes), stream=s_swap)
+    idx = torch.from_numpy(gpu_tab).cuda()
+    snaps = []
+    for l in range(geo.num_planes):
+        dp.wait_flag(s_use, base + 4 * (len(ops) + l), 5)
+        with torch.cuda.stream(s_use):
+            snaps.append(cache.planes[l, idx].clone())
+    torch.cuda.synchronize()
+    assert words.tolist() == [5] * words.numel()
+    for l in range(geo.num_planes):
+        assert np.array_equal(snaps[l].cpu().numpy(), pattern[l, gpu_tab])
+    want = np.zeros_like(pattern)
+    orc.apply_plan("in", want, host_img, ops)
+    np.testing.assert_array_equal(cache.planes.cpu().numpy(), want)
+    with pytest.raises(ValueError):  # reserved field must be zero
+        from paper_2411_18424_b200 import _lib
+        import ctypes
+        bad = _lib.KvsSignals(None, None, None, 1, 7)
+        _lib.check(dp.lib.kvs_swap_signaled(dp.handle, 1, None, 0, 0, ctypes.byref(bad)))
+    host.close()

@@ -166,3 +166,24 @@ def test_kv_token_kernel_matches_torch_pattern(cuda_ok, geo_name):
     with pytest.raises(IndexError):
         rt.dataplane.kv_tokens(0, np.array([[0, 0, 32, G - 1]]), stream=s)
     rt.close()
+
+
+def test_live_engine_layered_admission_bytes(cuda_ok):
+    """Layered admission: resumed requests join decode layer by layer (plane
+    flags); every joined request's KV is verified after its layers landed."""
+    from paper_2411_18424_b200.live import DecodeEmulator, LiveEngine, b200_transfer_params
+
+    convs = generate(WorkloadConfig(num_conversations=10, seed=5, max_context_tokens=2048,
+                                    arrival_rate_per_s=20.0, think_time_mean_s=0.05))
+    cfg = EngineConfig(gpu_pool=PoolConfig(total_blocks=128, initial_group_blocks=40),
+                       trace=PriorityTrace(pattern="random", frequency=0.04, seed=2),
+                       ablation="full", cpu_pool_blocks=4096, transfer=b200_transfer_params())
+    rt = _runtime(cfg, timing=True, layered_swap_in=True)
+    dec = DecodeEmulator("cuda:0", weight_bytes=1 << 30)
+    eng = LiveEngine(cfg, convs, rt, dec, layered=True)
+    rep = eng.run()
+    lat = eng.latency_summary()
+    assert rep.total_tokens == rep.expected_tokens
+    assert eng.layered_joins > 0 and rt.verified > 0
+    assert lat["layered_joins"] == eng.layered_joins
+    rt.close()

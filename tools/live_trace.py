@@ -37,8 +37,8 @@ def run_one(args, mode, impl, decode, geo):
     cfg = type(cfg)(**{**cfg.__dict__, "transfer": b200_transfer_params(args.pcie_gbs)})
     rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, copy_impl=impl,
                  verify=args.verify, timing=True, duplex_policy=args.policy,
-                 sm_partition=args.sm_partition)
-    eng = LiveEngine(cfg, generate(wl), rt, decode)
+                 sm_partition=args.sm_partition, layered_swap_in=args.layered)
+    eng = LiveEngine(cfg, generate(wl), rt, decode, layered=args.layered and impl == "kernel")
     eng.turn_trace = []
     t0 = time.perf_counter()
     rep = eng.run()
@@ -91,6 +91,8 @@ def main():
     ap.add_argument("--policy", default="latency")
     ap.add_argument("--sm-partition", type=int, default=0,
                     help="swap kernels on their own N-SM green context, decode on the rest")
+    ap.add_argument("--layered", action="store_true",
+                    help="resumed requests join decode layer by layer (plane flags)")
     ap.add_argument("--out", default="gpurun_out/live_trace.json")
     args = ap.parse_args()
     geo = PRESETS[args.model]
