@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace-convs", type=int, default=64)
     ap.add_argument("--no-trace", action="store_true")
+    ap.add_argument("--no-layered", action="store_true",
+                    help="trace: resumed requests join only once all their KV landed")
     ap.add_argument("--sm-partition", type=int, default=8,
                     help="serving + trace: swap kernels on their own N-SM green context, "
                          "decode on the rest (0 = share all SMs)")
@@ -479,9 +481,11 @@ def run_trace(args, geo, dev):
                              ("vllm_like", "baseline", "ce_per_block")):
         cfg, wl, _ = mconfig.build({**doc, "ablation": mode})
         cfg = dataclasses.replace(cfg, transfer=b200_transfer_params())
+        layered = impl == "kernel" and not args.no_layered
         rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, device=dev,
-                     copy_impl=impl, timing=True, sm_partition=args.sm_partition)
-        eng = LiveEngine(cfg, generate(wl), rt, decode, agreement=agreement)
+                     copy_impl=impl, timing=True, sm_partition=args.sm_partition,
+                     layered_swap_in=layered)
+        eng = LiveEngine(cfg, generate(wl), rt, decode, agreement=agreement, layered=layered)
         eng.turn_trace = []
         rep = eng.run()
         lat = eng.latency_summary()
@@ -493,6 +497,7 @@ def run_trace(args, geo, dev):
                                                     "swap_induced_decode_stall", "wall_s")},
                              "ttft_tail_ms": {"turns": anat.get("turns"),
                                               **anat.get("tail_mean_ms", {})},
+                             "layered_joins": lat["layered_joins"],
                              "tokens": rep.total_tokens,
                              "swap_gib": {"out": round(st["bytes_out"] / 2**30, 2),
                                           "in": round(st["bytes_in"] / 2**30, 2)},
