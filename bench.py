@@ -319,6 +319,16 @@ def run_ours(args, geo):
     if rank == 0 and not args.no_sweep:
         sweep = group_sweep(dp, s)
 
+    # ---- the SM partition is an optimisation: fall back to shared SMs if the
+    #      driver cannot create green contexts on this box ----
+    if args.sm_partition:
+        from paper_2411_18424_b200.swap import partition_streams
+        try:
+            partition_streams(dev, args.sm_partition)
+        except (RuntimeError, ValueError) as exc:
+            print(f"bench: SM partition unavailable ({exc}); sharing all SMs", file=sys.stderr)
+            args.sm_partition = 0
+
     # ---- serving configuration: paced swaps under a concurrent decode load ----
     serving = serving_interference(dp, dev, s) if rank == 0 else None
     if rank == 0 and args.sm_partition:
