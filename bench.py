@@ -560,13 +560,15 @@ def serving_interference(dp, dev, s, sm_partition: int = 0):
     ev = steps(20)
     torch.cuda.synchronize()
     solo = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(20))
-    pol = DUPLEX_POLICIES["latency"]
+    policy = os.environ.get("KVS_SERVING_POLICY", "latency")
+    pol = DUPLEX_POLICIES[policy]
     for d in ("out", "in"):
         c, t, pace = pol[d]
         dp.set_launch(d, c, t)
         dp.set_pace(d, pace)
     dp.set_budget(pol["budget"])
-    out = {"policy": "latency", "sm_partition": sms, "decode_step_solo_ms": round(solo, 3),
+    dp.set_budget_priority(pol.get("priority"))
+    out = {"policy": policy, "sm_partition": sms, "decode_step_solo_ms": round(solo, 3),
            "runs": {}}
     for name, dirs in (("out", ("out",)), ("in", ("in",)), ("duplex", ("out", "in"))):
         torch.cuda.synchronize()
@@ -592,6 +594,7 @@ def serving_interference(dp, dev, s, sm_partition: int = 0):
         dp.set_launch(d, 0, 0)
         dp.set_pace(d, 0.0)
     dp.set_budget(0.0)
+    dp.set_budget_priority(None)
     del dec
     return out
 

@@ -115,6 +115,13 @@ int kvs_set_pace(KvsHandle* h, int dir, double gbps);
  * more host-link traffic than decode tolerates. */
 int kvs_set_budget(KvsHandle* h, double gbps);
 
+/* Strict priority inside the shared budget: direction `dir` (or -1 = none)
+ * charges the budget without waiting for it, so the other direction gets
+ * only what is left.  Serving gives swap-in priority: it gates resumption
+ * (engine.py:376-384), while a swap-out's freed blocks are merely busy
+ * (engine.py:609, conflicts resolved per op). */
+int kvs_set_budget_priority(KvsHandle* h, int dir);
+
 /* Queue one SwapPlan's bytes on `stream` — asynchronous, no host blocking,
  * no allocation.  Replaces the modeled copy-engine timeline of
  * SwapManager.dispatch (swap.py:193-205, costmodel.py:29-31).

@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = (
     "kvs_set_path",
     "kvs_set_pace",
     "kvs_set_budget",
+    "kvs_set_budget_priority",
     "kvs_swap",
     "kvs_swap_layered",
     "kvs_swap_ops",
@@ -115,6 +116,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_set_pace.argtypes = [c.c_void_p, c.c_int, c.c_double]
     lib.kvs_set_budget.restype = c.c_int
     lib.kvs_set_budget.argtypes = [c.c_void_p, c.c_double]
+    lib.kvs_set_budget_priority.restype = c.c_int
+    lib.kvs_set_budget_priority.argtypes = [c.c_void_p, c.c_int]
     lib.kvs_swap.restype = c.c_int
     lib.kvs_swap.argtypes = [
         c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64, c.c_void_p, c.c_uint32,

@@ -72,6 +72,7 @@ struct SwapParams {
   unsigned long long* bucket;  // shared (both directions) budget clock, ns
   uint64_t bucket_cost_ns;     // >0: ns of budget one piece consumes
   uint64_t bucket_burst_ns;    // idle credit cap
+  uint32_t bucket_nowait;      // 1: charge the shared budget but never wait (priority side)
   int32_t op_end[CAP];         // inclusive prefix sum of TransferOp.blocks
   int32_t op_gpu[CAP];         // TransferOp.gpu_start
   int32_t op_cpu[CAP];         // TransferOp.cpu_start
@@ -186,10 +187,12 @@ __global__ void __launch_bounds__(kMaxThreads)
     if (p.bucket_cost_ns != 0) {
       // Shared budget: swap-out and swap-in of this handle together stay
       // under one rate, whatever their mix (a token bucket on a global clock).
+      // The priority direction only charges it; the other one waits its turn.
       unsigned long long slot = 0;
       if (lane == 0) slot = take_budget(p.bucket, p.bucket_cost_ns, p.bucket_burst_ns);
       slot = __shfl_sync(0xffffffffu, slot, 0);
-      while (globaltimer_ns() < slot) __nanosleep(64);
+      if (!p.bucket_nowait)
+        while (globaltimer_ns() < slot) __nanosleep(64);
     }
     const int64_t rel = static_cast<int64_t>(k) - op_begin;
     const int64_t off = static_cast<int64_t>(piece) * kPieceBytes;
@@ -371,7 +374,8 @@ __global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant
       if (p.bucket_cost_ns != 0) {
         const unsigned long long slot = take_budget(p.bucket, p.bucket_cost_ns,
                                                     p.bucket_burst_ns);
-        while (globaltimer_ns() < slot) __nanosleep(64);
+        if (!p.bucket_nowait)
+          while (globaltimer_ns() < slot) __nanosleep(64);
       }
     };
     const uint32_t pre = n < S - 1 ? n : S - 1;
@@ -442,6 +446,7 @@ struct KvsHandle {
   int stages[2] = {0, 0};
   uint64_t pace_ps[2] = {0, 0};  // per 4 KiB piece; 0 = unpaced
   double budget_gbps = 0.0;      // shared by both directions; 0 = none
+  int budget_priority = -1;      // direction that charges the budget without waiting
   unsigned long long* d_bucket = nullptr;
   int64_t launches = 0;
 };
@@ -532,6 +537,7 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
       h->budget_gbps > 0.0 ? static_cast<uint64_t>(piece / h->budget_gbps + 0.5) : 0;
   if (p.bucket_cost_ns == 0 && h->budget_gbps > 0.0) p.bucket_cost_ns = 1;
   p.bucket_burst_ns = 16 * p.bucket_cost_ns;
+  p.bucket_nowait = h->budget_priority == dir ? 1u : 0u;
   if (o.op_flags != nullptr) {
     // Same stream as the kernel: ordered before it, and after the previous
     // launch of this direction that used the counters.
@@ -693,6 +699,13 @@ int kvs_set_pace(KvsHandle* h, int dir, double gbps) {
 int kvs_set_budget(KvsHandle* h, double gbps) {
   if (h == nullptr || !(gbps >= 0.0) || gbps > 1e6) return KVS_ERR_INVALID;
   h->budget_gbps = gbps;
+  return KVS_OK;
+}
+
+int kvs_set_budget_priority(KvsHandle* h, int dir) {
+  if (h == nullptr || (dir != -1 && dir != KVS_DIR_OUT && dir != KVS_DIR_IN))
+    return KVS_ERR_INVALID;
+  h->budget_priority = dir;
   return KVS_OK;
 }
 

@@ -227,6 +227,11 @@ class SwapDataPlane:
         """One GB/s budget shared by swap-out and swap-in (0 = none)."""
         _lib.check(self.lib.kvs_set_budget(self.handle, float(gbps)), "kvs_set_budget")
 
+    def set_budget_priority(self, direction: Optional[str]) -> None:
+        """Direction that charges the shared budget without waiting (None = neither)."""
+        d = -1 if direction is None else _lib.DIRECTIONS[direction]
+        _lib.check(self.lib.kvs_set_budget_priority(self.handle, d), "kvs_set_budget_priority")
+
     @property
     def launches(self) -> int:
         return int(self.lib.kvs_launch_count(self.handle))

@@ -204,6 +204,9 @@ COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 #   unpaced    — out 8x512, in 32x512, no pacing (round-1 default shape).
 DUPLEX_POLICIES = {
     "latency": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0},
+    # same, but swap-in draws on the shared budget first (kvs_set_budget_priority)
+    "latency_in_first": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
+                         "priority": "in"},
     "throughput": {"out": (32, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
     "unpaced": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
 }
@@ -296,6 +299,7 @@ class StreamExecutor:
             self.dp.set_launch(direction, ctas, threads)
             self.dp.set_pace(direction, pace)
         self.dp.set_budget(pol["budget"])
+        self.dp.set_budget_priority(pol.get("priority"))
         self.duplex_policy = policy
 
     def _prune(self) -> None:
