@@ -372,6 +372,8 @@ def run_ours(args, geo):
             "roofline": {"bound": "pcie", "achieved": round(achieved, 3),
                          "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
                          "frac": round(achieved / PCIE_GEN5_X16_GBS, 4), "traffic": traffic,
+                         "aggregate": {"gbs": round(value, 3), "links": world,
+                                       "frac": round(value / (world * PCIE_GEN5_X16_GBS), 4)},
                          "kernel": f"kvs_swap_kernel<{dominant}>",
                          "peak_source": "PCIe Gen5 x16 per direction after 128b/130b "
                                         "(BASELINE.md §4; MEASURED_PEAKS.json has no PCIe entry)",
