@@ -339,7 +339,7 @@ def run_ours(args, geo):
     # ---- live multi-turn preemption trace: P99 TTFT / TBT (metric part 2) ----
     trace = None
     if not args.no_trace:
-        host.close()  # free the 16 GiB pinned pool before the trace's own pools
+        host.close()  # free the 10 GiB pinned pool before the trace's own pools
         trace = run_trace(args, geo, dev)
 
     cpu = None
@@ -349,6 +349,10 @@ def run_ours(args, geo):
         cpu = {"value": round(rate, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                "sample": sample, "cpu_model": cpu_model()}
 
+    numa_per_rank = [host_numa]
+    if world > 1:  # where each rank's swap space lives (NUMA node of its GPU)
+        numa_per_rank = [None] * world
+        dist.all_gather_object(numa_per_rank, host_numa)
     if rank == 0:
         dominant, dom_ms = ("in", in_ms) if sum(in_ms) >= sum(out_ms) else ("out", out_ms)
         achieved = nbytes_dir / (statistics.mean(dom_ms) * 1e-3) / 1e9
@@ -367,6 +371,7 @@ def run_ours(args, geo):
                        "parallelism": f"replicas{world} (per-rank KV shard, own PCIe link)",
                        "l2": "inputs 8 GiB/direction > 126 MB L2, no flush",
                        "host_pool": {"blocks": HOST_POOL_BLOCKS, "numa_node": host_numa,
+                                     "numa_node_per_rank": numa_per_rank,
                                      "numa_nodes": numa_nodes()}},
             "per_direction_gbs": {"out": round(out_gbs, 3), "in": round(in_gbs, 3)},
             "roofline": {"bound": "pcie", "achieved": round(achieved, 3),

@@ -21,7 +21,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, layered=False):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
@@ -45,9 +45,10 @@ def _worker(rank, world, port, q):
                            trace=PriorityTrace(pattern="random", frequency=0.04, seed=2),
                            ablation="full", cpu_pool_blocks=2048,
                            transfer=b200_transfer_params())
-        rt = Runtime(geo, 128, 2048, device="cuda:0", verify=True, timing=True)
+        rt = Runtime(geo, 128, 2048, device="cuda:0", verify=True, timing=True,
+                     layered_swap_in=layered)
         dec = DecodeEmulator("cuda:0", weight_bytes=1 << 30)
-        eng = LiveEngine(cfg, convs, rt, dec, agreement=RankAgreement())
+        eng = LiveEngine(cfg, convs, rt, dec, agreement=RankAgreement(), layered=layered)
         dig = multirank.PlanDigest().attach(eng.manager)
         rep = eng.run()
         q.put((rank, dig.hexdigest(), dig.plans, list(eng.ttft_samples),
@@ -58,12 +59,14 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_tp_ranks_decide_in_lockstep(cuda_ok):
+@pytest.mark.parametrize("layered", [False, True])
+def test_two_tp_ranks_decide_in_lockstep(cuda_ok, layered):
     world = 2
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, layered))
+             for r in range(world)]
     for p in procs:
         p.start()
     got = sorted(q.get(timeout=600) for _ in range(world))
