@@ -386,7 +386,8 @@ def run_ours(args, geo):
                          "frac_of_ce": {d: round((out_gbs if d == "out" else in_gbs) / ce[d], 4)
                                         for d in ("out", "in")} if ce else None,
                          "hbm": {"achieved": round(achieved, 3),
-                                 "peak": measured_hbm_peak(), "unit": "GB/s"}},
+                                 "peak": measured_hbm_peak(), "unit": "GB/s"},
+                         "ncu": ncu_link_rates()},
             "e2e": e2e,
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
@@ -674,6 +675,20 @@ def ncu_traffic(direction: str):
         return d["kernels"][direction]["dram_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
         return None
+
+
+def ncu_link_rates():
+    """Host-link and HBM rates of both swap kernels from the committed ncu
+    capture (profiles/ncu_kernel_summary.json): payload vs wire bytes."""
+    try:
+        d = json.load(open(ROOT / "profiles" / "ncu_kernel_summary.json"))
+    except (OSError, ValueError):
+        return None
+    out = {"source": d.get("source")}
+    for k, v in d.get("kernels", {}).items():
+        out[k] = {"pcie_write_gbs": v.get("pcie_write_gbs"), "pcie_read_gbs": v.get("pcie_read_gbs"),
+                  "dram_gbs": v.get("dram_gbs"), "duration_s": v.get("duration_s")}
+    return out
 
 
 def main():
