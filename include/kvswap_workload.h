@@ -32,15 +32,17 @@ int kvs_stream_read(int device, uint64_t stream, const void* buf, size_t buf_byt
  * (int64 x4 each: request, first token, end token, physical block holding the
  * first token; a segment's tokens sit in physically consecutive blocks of
  * `block_tokens` slots), write (mode 0) or compare (mode 1) the token's
- * deterministic K and V rows in every plane of `h`'s paged cache
- * ([2][block_tokens][row] per plane chunk), on `stream`.  Stand-in for the KV
- * that attention appends each iteration; mode 1 adds the number of differing
- * 32-bit words to *mismatch (device memory).  Word w of plane p, K/V kv of
+ * deterministic K and V rows in planes [plane_lo, plane_hi) (plane_hi = -1:
+ * all) of `h`'s paged cache ([2][block_tokens][row] per plane chunk), on
+ * `stream`.  Mode 0 stands in for the KV attention appends each iteration;
+ * mode 1 for attention reading the batch's KV, adding the number of
+ * differing 32-bit words to *mismatch (device memory).  Word w of plane p, K/V kv of
  * token t of request r is t*0x01000193 + r*0x5BD1E995 + p*0x9E3779B1 +
  * kv*0x7F4A7C15 + w (mod 2^32). */
 typedef struct KvsHandle KvsHandle;
 int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_t n_segs,
-                  int32_t block_tokens, uint64_t stream, uint32_t* mismatch);
+                  int32_t block_tokens, int32_t plane_lo, int32_t plane_hi, uint64_t stream,
+                  uint32_t* mismatch);
 
 #ifdef __cplusplus
 }

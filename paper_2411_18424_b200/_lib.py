@@ -157,7 +157,7 @@ def _declare(lib: ctypes.CDLL) -> None:
                                     c.c_int, c.c_void_p]
     lib.kvs_kv_tokens.restype = c.c_int
     lib.kvs_kv_tokens.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_int32,
-                                  c.c_uint64, c.c_void_p]
+                                  c.c_int32, c.c_int32, c.c_uint64, c.c_void_p]
 
 
 def load(path: Optional[os.PathLike] = None) -> ctypes.CDLL:

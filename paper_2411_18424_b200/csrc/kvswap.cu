@@ -1066,16 +1066,17 @@ constexpr int kTokSegsMax = 256;
 struct TokSegs {
   const uint64_t* planes;
   int64_t stride;          // plane_block_stride
-  uint32_t num_planes;
+  uint32_t plane_lo;       // planes [plane_lo, plane_lo + n_planes)
+  uint32_t n_planes;
   uint32_t block_tokens;
   uint32_t words;          // int32 words per (K or V) token row
   uint32_t n_segs;
   uint32_t* mismatch;      // mode 1: count of mismatching words
   int32_t mode;            // 0 write, 1 check
   uint32_t seg_req[kTokSegsMax];
-  int32_t seg_lo[kTokSegsMax];     // first token
+  int32_t seg_lo[kTokSegsMax];       // first token
   int32_t seg_tok_end[kTokSegsMax];  // inclusive prefix sum of tokens
-  int32_t seg_phys[kTokSegsMax];   // physical block of token seg_lo
+  int32_t seg_phys[kTokSegsMax];     // physical block of token seg_lo
 };
 
 // Runtime._pattern restated in uint32 (identical mod 2^32).
@@ -1084,20 +1085,24 @@ __device__ __forceinline__ uint32_t kv_word(uint32_t req, uint32_t tok, uint32_t
   return tok * 0x01000193u + req * 0x5BD1E995u + plane * 0x9E3779B1u + kv * 0x7F4A7C15u + w;
 }
 
-// One warp per (token, plane, kv) row; lanes stride the row's words.
+// One warp per (token, plane, K/V) row; lanes move 16 B vectors when the row
+// allows (word counts % 4 == 0), else single words.  Mode 1 is the live
+// engine's attention stand-in: it reads every KV byte of the batch and counts
+// words that differ from what the tokens wrote.
 __global__ void __launch_bounds__(256) kvs_kv_tokens_kernel(const __grid_constant__ TokSegs s) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint32_t total_tokens = static_cast<uint32_t>(s.seg_tok_end[s.n_segs - 1]);
-  const uint64_t rows = static_cast<uint64_t>(total_tokens) * s.num_planes * 2u;
+  const uint64_t rows = static_cast<uint64_t>(total_tokens) * s.n_planes * 2u;
+  const bool vec = (s.words & 3u) == 0;
   uint32_t bad = 0;
   uint32_t seg = 0;
   for (uint64_t r = warp; r < rows; r += nwarps) {
     const uint32_t kv = static_cast<uint32_t>(r & 1u);
     const uint64_t rp = r >> 1;
-    const uint32_t plane = static_cast<uint32_t>(rp % s.num_planes);
-    const uint32_t i = static_cast<uint32_t>(rp / s.num_planes);  // flat token index
+    const uint32_t plane = s.plane_lo + static_cast<uint32_t>(rp % s.n_planes);
+    const uint32_t i = static_cast<uint32_t>(rp / s.n_planes);  // flat token index
     while (static_cast<int32_t>(i) >= s.seg_tok_end[seg]) ++seg;
     const int32_t seg_begin = seg == 0 ? 0 : s.seg_tok_end[seg - 1];
     const uint32_t tok = static_cast<uint32_t>(s.seg_lo[seg] + (static_cast<int32_t>(i) - seg_begin));
@@ -1108,7 +1113,18 @@ __global__ void __launch_bounds__(256) kvs_kv_tokens_kernel(const __grid_constan
         reinterpret_cast<char*>(__ldg(s.planes + plane)) + static_cast<int64_t>(blk) * s.stride) +
         (static_cast<uint64_t>(kv) * s.block_tokens + slot) * s.words;
     const uint32_t base = kv_word(s.seg_req[seg], tok, plane, kv, 0);
-    if (s.mode == 0) {
+    if (vec) {
+      uint4* row4 = reinterpret_cast<uint4*>(row);
+      for (uint32_t w = lane; w < s.words / 4; w += 32) {
+        const uint32_t b0 = base + 4 * w;
+        if (s.mode == 0) {
+          row4[w] = make_uint4(b0, b0 + 1, b0 + 2, b0 + 3);
+        } else {
+          const uint4 v = row4[w];
+          bad += (v.x != b0) + (v.y != b0 + 1) + (v.z != b0 + 2) + (v.w != b0 + 3);
+        }
+      }
+    } else if (s.mode == 0) {
       for (uint32_t w = lane; w < s.words; w += 32) row[w] = base + w;
     } else {
       for (uint32_t w = lane; w < s.words; w += 32) bad += row[w] != base + w;
@@ -1123,9 +1139,13 @@ __global__ void __launch_bounds__(256) kvs_kv_tokens_kernel(const __grid_constan
 }  // namespace
 
 extern "C" int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_t n_segs,
-                             int32_t block_tokens, uint64_t stream, uint32_t* mismatch) {
+                             int32_t block_tokens, int32_t plane_lo, int32_t plane_hi,
+                             uint64_t stream, uint32_t* mismatch) {
   if (h == nullptr || (mode != 0 && mode != 1) || n_segs < 0 || block_tokens < 1 ||
       (n_segs > 0 && segs == nullptr) || (mode == 1 && mismatch == nullptr))
+    return KVS_ERR_INVALID;
+  if (plane_hi < 0) plane_hi = h->geo.num_planes;  // -1: every plane
+  if (plane_lo < 0 || plane_lo >= plane_hi || plane_hi > h->geo.num_planes)
     return KVS_ERR_INVALID;
   const int64_t chunk = h->geo.plane_chunk_bytes;
   if (chunk % (2 * block_tokens * 4)) return KVS_ERR_INVALID;
@@ -1136,7 +1156,8 @@ extern "C" int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_
     TokSegs s{};
     s.planes = h->d_planes;
     s.stride = h->geo.plane_block_stride;
-    s.num_planes = static_cast<uint32_t>(h->geo.num_planes);
+    s.plane_lo = static_cast<uint32_t>(plane_lo);
+    s.n_planes = static_cast<uint32_t>(plane_hi - plane_lo);
     s.block_tokens = static_cast<uint32_t>(block_tokens);
     s.words = static_cast<uint32_t>(chunk / (2 * block_tokens * 4));
     s.mismatch = mismatch;
@@ -1160,7 +1181,7 @@ extern "C" int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_
     }
     if (n == 0) continue;
     s.n_segs = n;
-    const uint64_t rows = static_cast<uint64_t>(tokens) * s.num_planes * 2;
+    const uint64_t rows = static_cast<uint64_t>(tokens) * s.n_planes * 2;
     const uint64_t want = (rows + 7) / 8;  // 8 warps per CTA
     const int ctas = static_cast<int>(want < 1184 ? want : 1184);
     kvs_kv_tokens_kernel<<<ctas, 256, 0, st>>>(s);

@@ -296,12 +296,14 @@ class SwapDataPlane:
         _lib.check(rc, f"kvs_memcpy_baseline({direction}, mode={mode})")
 
     def kv_tokens(self, mode: int, segs: np.ndarray, stream: Optional[torch.cuda.Stream] = None,
-                  mismatch_ptr: int = 0) -> None:
+                  mismatch_ptr: int = 0, planes: Optional[tuple[int, int]] = None) -> None:
         """Write (mode 0) or check (mode 1) the synthetic KV of token segments
-        int64 [n, 4] = (request, lo, hi, physical block of token lo)."""
+        int64 [n, 4] = (request, lo, hi, physical block of token lo), in
+        planes [lo, hi) (default: all)."""
         arr = np.ascontiguousarray(segs, dtype=np.int64).reshape(-1, 4)
+        p_lo, p_hi = planes if planes is not None else (0, -1)
         rc = self.lib.kvs_kv_tokens(self.handle, mode, arr.ctypes.data_as(ctypes.c_void_p),
-                                    arr.shape[0], self.geometry.block_tokens,
+                                    arr.shape[0], self.geometry.block_tokens, p_lo, p_hi,
                                     _stream_handle(stream),
                                     ctypes.c_void_p(mismatch_ptr) if mismatch_ptr else None)
         _lib.check(rc, "kvs_kv_tokens")

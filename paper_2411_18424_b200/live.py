@@ -168,13 +168,18 @@ class LiveEngine(Engine):
 
     def __init__(self, config: EngineConfig, conversations, runtime, decode: DecodeEmulator,
                  time_scale: float = 1.0, agreement: Optional[RankAgreement] = None,
-                 layered: bool = False) -> None:
+                 layered: bool = False, attend: bool = True) -> None:
         """layered: resumed requests join decode layer by layer (SURVEY §8f
         rank 2).  A swap-in at the head of the swap-in stream whose modeled
         completion falls inside this iteration joins the batch now, and so do
         sync-mode swap-ins (swap.py:113-135); decode layer l waits only for
         layer l of their KV (plane flags), instead of the reference's
-        iteration-wise completion (engine.py:376-384)."""
+        iteration-wise completion (engine.py:376-384).
+
+        attend: each iteration also reads (and checks) the resident KV of
+        every computing request, as attention would, inside the iteration's
+        modeled time; any byte that differs from what its token wrote fails
+        the run (runtime.KVIntegrityError)."""
         if runtime is None:
             raise ValueError("live mode needs a Runtime (real data plane)")
         super().__init__(config, conversations, runtime=runtime)
@@ -187,6 +192,7 @@ class LiveEngine(Engine):
                              "with the kernel copy path")
         self._deferred: Optional[list] = None
         self.layered_joins = 0
+        self.attend = attend and runtime.write_kv
         self.live = LiveStats()
         # per computing iteration: (duration_us, cpu_us, wait_ms, kernel_ms,
         #                           synced, conflict_waits, n_prefill, n_decode)
@@ -410,10 +416,18 @@ class LiveEngine(Engine):
             t_cpu = time.perf_counter()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
+            # The step's modeled time is spent reading the batch's KV
+            # (attention) and streaming weights for the rest.
+            reads = spans if self.attend else []
+            kv_bytes = sum(lo for _, lo, _ in reads) * self.runtime.token_bytes
+            w_us = max(0.0, nominal_us - kv_bytes / self.decode.bytes_per_us)
             if layer_deps:
                 # Decode layer by layer; layer l waits for layer l of every
                 # joining request's KV.  This iteration's KV writes follow the
                 # last layer, when every joining request's KV has landed.
+                self.runtime.barrier(self, spans, skip=layer_deps)
+                t_rt = time.perf_counter()
+                waits_seen = grant_waits + list(ex.last_barrier)
                 swapping = True
                 e0.record(compute)
                 planes = self.runtime.geometry.num_planes
@@ -421,18 +435,21 @@ class LiveEngine(Engine):
                 for layer in range(planes):
                     for dep in layer_deps:
                         ex.wait_plane(compute, dep, layer)
-                    nbytes += self.decode.launch_us(compute, nominal_us / planes)
+                    if reads:
+                        nbytes += self.runtime.attend(self, reads, planes=(layer, layer + 1))
+                    if w_us > 0:
+                        nbytes += self.decode.launch_us(compute, w_us / planes)
                 e1.record(compute)
-                self.runtime.compute(self, spans, skip=layer_deps)
-                t_rt = time.perf_counter()
-                waits_seen = grant_waits + list(ex.last_barrier)
+                self.runtime.write(self, spans)
             else:
                 self.runtime.compute(self, spans)
                 t_rt = time.perf_counter()
                 waits_seen = grant_waits + list(ex.last_barrier)
                 e0.record(compute)
                 swapping = any(not r.poll() for r in ex.pending)
-                nbytes = self.decode.launch_us(compute, nominal_us)
+                nbytes = self.runtime.attend(self, reads) if reads else 0
+                if w_us > 0:
+                    nbytes += self.decode.launch_us(compute, w_us)
                 e1.record(compute)
             compute.synchronize()
             if self._deferred:
@@ -485,6 +502,12 @@ class LiveEngine(Engine):
 
         self.runtime.synchronize()
         self.live.wall_s = time.perf_counter() - wall0
+        if self.attend:
+            bad = self.runtime.kv_errors()
+            if bad:
+                from .runtime import KVIntegrityError
+                raise KVIntegrityError(f"{bad} KV words read by decode differ from what their "
+                                       f"tokens wrote")
         return self._report(stalls, self._efficiencies(windows), first_arrival)
 
     def spike_breakdown(self, q: float = 0.99) -> dict:
@@ -527,6 +550,7 @@ class LiveEngine(Engine):
             "iterations": self.live.iterations,
             "idle_waits": self.live.idle_waits,
             "layered_joins": self.layered_joins,
+            "kv_read_gib": round(self.runtime.kv_bytes_read / 2**30, 2),
             "wall_s": round(self.live.wall_s, 2),
             "slow_iterations": self.spike_breakdown(),
             "tp_agreement": None if self.agreement is None else {

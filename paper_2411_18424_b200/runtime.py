@@ -94,6 +94,8 @@ class Runtime:
         self._word_term = torch.arange(self._words, device=dev, dtype=torch.int64).view(
             1, 1, 1, -1)
         self._mismatch = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._kv_bad = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.kv_bytes_read = 0
 
     # -- token KV pattern -----------------------------------------------------
 
@@ -113,16 +115,49 @@ class Runtime:
         """One iteration's compute on the compute stream: wait for conflicting
         transfers (except `skip`, already waited for per layer), then write
         the KV of every produced token (one launch)."""
+        self.barrier(engine, spans, skip)
+        self.write(engine, spans)
+
+    def barrier(self, engine, spans, skip=()) -> None:
         extents = []
         for req, _, _ in spans:
             extents.extend(engine._gpu_extents(req))
         self.barrier_waits += self.executor.compute_barrier(extents, skip=skip)
+
+    def write(self, engine, spans) -> None:
         if not self.write_kv:
             return
         segs = self.segments(engine, spans)
         if len(segs):
             self.dataplane.kv_tokens(0, segs, stream=self.executor.compute)
             self.tokens_written += int((segs[:, 2] - segs[:, 1]).sum())
+
+    @property
+    def token_bytes(self) -> int:
+        """KV bytes of one token across all planes (K and V)."""
+        return self.geometry.block_bytes // self.geometry.block_tokens
+
+    def attend(self, engine, spans, planes: Optional[tuple[int, int]] = None) -> int:
+        """Attention stand-in: read (and check) the resident KV of every
+        computing request, tokens [0, lo) of each span, in `planes`; returns
+        the bytes read.  Mismatches accumulate on the device (kv_errors())."""
+        if not self.write_kv:
+            return 0
+        segs = self.segments(engine, [(req, 0, lo) for req, lo, _ in spans])
+        if not len(segs):
+            return 0
+        self.dataplane.kv_tokens(1, segs, stream=self.executor.compute,
+                                 mismatch_ptr=self._kv_bad.data_ptr(), planes=planes)
+        tokens = int((segs[:, 2] - segs[:, 1]).sum())
+        n = self.geometry.num_planes if planes is None else planes[1] - planes[0]
+        nbytes = tokens * self.token_bytes * n // self.geometry.num_planes
+        self.kv_bytes_read += nbytes
+        return nbytes
+
+    def kv_errors(self) -> int:
+        """Words that differed from their tokens' KV in every attend() so far."""
+        self.executor.compute.synchronize()
+        return int(self._kv_bad.item())
 
     def swap_in_landed(self, engine, req: int) -> None:
         if not self.verify:
@@ -156,6 +191,7 @@ class Runtime:
         return {"bytes_out": ex.bytes["out"], "bytes_in": ex.bytes["in"],
                 "refresh_bytes": ex.refresh_bytes, "kernel_launches": ex.launches,
                 "tokens_written": self.tokens_written, "verified_swap_ins": self.verified,
+                "kv_bytes_read": self.kv_bytes_read,
                 "compute_waits": self.barrier_waits}
 
     def close(self) -> None:

@@ -121,6 +121,7 @@ def test_live_engine_bytes_and_latency(cuda_ok):
     assert rep.swap_out_blocks > 0 and rt.verified > 0
     assert lat["ttft_p99_ms"] is not None and lat["tbt_p99_ms"] > 0
     assert dec.bytes_per_us > 1e6  # > 1 TB/s calibrated weight streaming
+    assert rt.kv_bytes_read > 0 and rt.kv_errors() == 0  # decode read every resident KV byte
     rt.close()
 
 
@@ -186,4 +187,36 @@ def test_live_engine_layered_admission_bytes(cuda_ok):
     assert rep.total_tokens == rep.expected_tokens
     assert eng.layered_joins > 0 and rt.verified > 0
     assert lat["layered_joins"] == eng.layered_joins
+    assert rt.kv_bytes_read > 0 and rt.kv_errors() == 0
+    rt.close()
+
+
+def test_live_attention_reads_catch_corruption(cuda_ok):
+    """The attention stand-in checks every resident KV byte it reads: a byte
+    flipped in a running request's block fails the run."""
+    import torch
+
+    from paper_2411_18424_b200.live import DecodeEmulator, LiveEngine, b200_transfer_params
+    from paper_2411_18424_b200.runtime import KVIntegrityError
+
+    convs = [Conversation(0, [(320, 200)], 0, 0)]
+    cfg = EngineConfig(gpu_pool=PoolConfig(total_blocks=64, initial_group_blocks=40),
+                       trace=PriorityTrace(pattern="random", frequency=0.04, seed=2),
+                       ablation="full", cpu_pool_blocks=256, transfer=b200_transfer_params())
+    rt = _runtime(cfg)
+    dec = DecodeEmulator("cuda:0", weight_bytes=1 << 30)
+    eng = LiveEngine(cfg, convs, rt, dec)
+    writes = {"n": 0}
+    orig = rt.write
+
+    def corrupting_write(engine, spans):
+        orig(engine, spans)
+        writes["n"] += 1
+        if writes["n"] == 20:  # after a few decode steps: flip one word of token 3's K row
+            start, _ = engine._gpu_extents(0)[0]
+            with torch.cuda.stream(rt.executor.compute):
+                rt._slots[0, start, 0, 3, 0] ^= 1
+    rt.write = corrupting_write
+    with pytest.raises(KVIntegrityError):
+        eng.run()
     rt.close()
