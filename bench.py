@@ -516,6 +516,7 @@ def run_trace(args, geo, dev):
                              "ttft_tail_ms": {"turns": anat.get("turns"),
                                               **anat.get("tail_mean_ms", {})},
                              "layered_joins": lat["layered_joins"],
+                             "kv_read_gib_verified": lat["kv_read_gib"],
                              "tokens": rep.total_tokens,
                              "swap_gib": {"out": round(st["bytes_out"] / 2**30, 2),
                                           "in": round(st["bytes_in"] / 2**30, 2)},
