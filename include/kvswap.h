@@ -64,6 +64,8 @@ extern "C" {
 /* kvs_host_alloc flags */
 #define KVS_HOST_DEFAULT 0
 #define KVS_HOST_REGISTER 1 /* mmap + (optional) mbind + cudaHostRegister instead of cudaHostAlloc */
+#define KVS_HOST_WRITE_COMBINED 2 /* cudaHostAlloc(...|WriteCombined): not snooped over PCIe;
+                                     slow for CPU reads (the pool is GPU-only traffic) */
 
 typedef struct KvsGeometry {
   int32_t num_planes;         /* P >= 1                                        */

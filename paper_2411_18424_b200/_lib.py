@@ -36,6 +36,7 @@ PATHS = {"lsu": KVS_PATH_LSU, "bulk": KVS_PATH_BULK}
 
 KVS_HOST_DEFAULT = 0
 KVS_HOST_REGISTER = 1
+KVS_HOST_WRITE_COMBINED = 2
 
 # Every symbol include/kvswap.h declares; tests assert all are exported.
 EXPORTED_SYMBOLS = (

@@ -893,8 +893,10 @@ int kvs_host_alloc(size_t bytes, int numa_node, int flags, void** host, void** d
   *host = nullptr;
   *dev = nullptr;
   void* p = nullptr;
-  if (flags == KVS_HOST_DEFAULT) {
-    int rc = cuda_rc(cudaHostAlloc(&p, bytes, cudaHostAllocMapped | cudaHostAllocPortable));
+  if (flags == KVS_HOST_DEFAULT || flags == KVS_HOST_WRITE_COMBINED) {
+    unsigned f = cudaHostAllocMapped | cudaHostAllocPortable;
+    if (flags == KVS_HOST_WRITE_COMBINED) f |= cudaHostAllocWriteCombined;
+    int rc = cuda_rc(cudaHostAlloc(&p, bytes, f));
     if (rc) return rc;
   } else if (flags == KVS_HOST_REGISTER) {
     p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
@@ -919,7 +921,7 @@ int kvs_host_alloc(size_t bytes, int numa_node, int flags, void** host, void** d
   void* d = nullptr;
   int rc = cuda_rc(cudaHostGetDevicePointer(&d, p, 0));
   if (rc) {
-    if (flags == KVS_HOST_DEFAULT) {
+    if (flags != KVS_HOST_REGISTER) {
       cudaFreeHost(p);
     } else {
       cudaHostUnregister(p);
@@ -945,7 +947,7 @@ int kvs_host_free(void* host) {
     a = it->second;
     g_host_allocs.erase(it);
   }
-  if (a.flags == KVS_HOST_DEFAULT) return cuda_rc(cudaFreeHost(host));
+  if (a.flags != KVS_HOST_REGISTER) return cuda_rc(cudaFreeHost(host));
   int rc = cuda_rc(cudaHostUnregister(host));
   munmap(host, a.bytes);
   return rc;

@@ -104,7 +104,7 @@ class HostKVPool:
     use cudaHostAlloc."""
 
     def __init__(self, num_blocks: int, block_bytes: int, numa_node: Optional[int] = -1,
-                 register: bool = False, device=None) -> None:
+                 register: bool = False, device=None, write_combined: bool = False) -> None:
         if num_blocks < 1 or block_bytes < 16 or block_bytes % 16:
             raise ValueError("host pool needs >= 1 block of a 16-byte multiple")
         lib = _lib.load()
@@ -117,7 +117,10 @@ class HostKVPool:
         self.nbytes = num_blocks * block_bytes
         host = ctypes.c_void_p()
         dev = ctypes.c_void_p()
-        flags = _lib.KVS_HOST_REGISTER if register else _lib.KVS_HOST_DEFAULT
+        if write_combined and register:
+            raise ValueError("write-combined pools come from cudaHostAlloc, not registration")
+        flags = (_lib.KVS_HOST_REGISTER if register else
+                 _lib.KVS_HOST_WRITE_COMBINED if write_combined else _lib.KVS_HOST_DEFAULT)
         _lib.check(lib.kvs_host_alloc(self.nbytes, numa_node, flags,
                                       ctypes.byref(host), ctypes.byref(dev)),
                    "kvs_host_alloc")
