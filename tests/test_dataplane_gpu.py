@@ -525,3 +525,35 @@ def test_signaled_swap_op_plane_and_done_flags(cuda_ok, n_ops_big):
         bad = _lib.KvsSignals(None, None, None, 1, 7)
         _lib.check(dp.lib.kvs_swap_signaled(dp.handle, 1, None, 0, 0, ctypes.byref(bad)))
     host.close()
+
+
+def test_split_kv_layout_vs_oracle(cuda_ok):
+    """vLLM-v0 style split K/V caches ([2, num_blocks, ...] per layer) are two
+    planes per layer; same block bytes as the fused layout, byte-exact."""
+    torch = cuda_ok
+    from paper_2411_18424_b200.geometry import KVGeometry
+
+    fused = KVGeometry("s", num_layers=4, num_kv_heads=2, head_dim=64)
+    geo = KVGeometry("s", num_layers=4, num_kv_heads=2, head_dim=64, split_kv=True)
+    assert geo.num_planes == 2 * fused.num_planes and geo.block_bytes == fused.block_bytes
+    G = C = 200
+    cache, host, dp = _mk(torch, geo, G, C)
+    rng = np.random.default_rng(17)
+    pattern = orc.kv_pattern(17, geo.num_planes, G, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    torch.cuda.synchronize()
+    ops = orc.table_to_ops(orc.random_block_table(rng, 150, G), orc.random_block_table(rng, 150, C))
+    host.array[:] = 0
+    dp.swap("out", ops)
+    torch.cuda.synchronize()
+    want = np.zeros((C, geo.block_bytes), np.uint8)
+    orc.apply_plan("out", pattern, want, ops)
+    np.testing.assert_array_equal(host.array, want)
+    cache.planes.zero_()
+    torch.cuda.synchronize()
+    dp.swap("in", ops)
+    torch.cuda.synchronize()
+    back = np.zeros_like(pattern)
+    orc.apply_plan("in", back, want, ops)
+    np.testing.assert_array_equal(cache.planes.cpu().numpy(), back)
+    host.close()
