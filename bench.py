@@ -411,7 +411,8 @@ def run_e2e(args, geo, dp, dev, barrier, world):
     from paper_2411_18424_b200.cpu_store import CpuStore
     from paper_2411_18424_b200.swap import StreamExecutor, SwapManager
 
-    ex = StreamExecutor(dp, duplex_policy="throughput")  # bulk round trip: max combined GB/s
+    # bulk round trip: the throughput policy (TMA bulk kernels both ways, plan-level waits)
+    ex = StreamExecutor(dp, duplex_policy="throughput")
     mgr = SwapManager(TransferParams(), bytes_per_block=geo.block_bytes, executor=ex)
     store = CpuStore(HOST_POOL_BLOCKS, reuse_enabled=True)
     n_req, per = 64, PLAN_BLOCKS // 64
@@ -454,10 +455,13 @@ def run_e2e(args, geo, dp, dev, barrier, world):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         el = float(t.item())
     moved = sum(foot) * geo.block_bytes
+    for d in ("out", "in"):
+        dp.set_path(d, "lsu")
     return {"value": round(world * 2 * moved * args.steps / el / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": moved, "d2h_bytes_per_step": moved,
             "api": "CpuStore.plan_swap_out/plan_swap_in -> SwapManager.dispatch -> "
-                   "StreamExecutor -> kvs_swap (C ABI); wall clock incl. planning and sync",
+                   "StreamExecutor (throughput policy: TMA bulk kernels) -> kvs_swap (C ABI); "
+                   "wall clock incl. planning and sync",
             "requests_per_step": n_req, "gpu_launches": launches}
 
 

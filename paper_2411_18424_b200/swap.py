@@ -199,15 +199,17 @@ COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 # (profiles/r01_interference_policy.json).
 #   latency    — serving: out 8x512 @52 GB/s, in 8x256 in-flight bound, both
 #                directions together capped at 60 GB/s (shared budget);
-#   throughput — bulk migration: unpaced, balanced 32x512 each way
-#                (highest combined GB/s, decode pays for it);
+#   throughput — bulk migration: unpaced TMA bulk kernels, 64 CTAs each way
+#                (both directions at once: 80 GB/s combined vs 75 with the
+#                LSU kernel, profiles/r01_duplex_mix.json; plan-level waits;
+#                decode pays for it);
 #   unpaced    — out 8x512, in 32x512, no pacing (round-1 default shape).
 DUPLEX_POLICIES = {
     "latency": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0},
     # same, but swap-in draws on the shared budget first (kvs_set_budget_priority)
     "latency_in_first": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
                          "priority": "in"},
-    "throughput": {"out": (32, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
+    "throughput": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0, "path": "bulk"},
     "unpaced": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
 }
 
@@ -270,9 +272,11 @@ class StreamExecutor:
             torch.cuda.Stream(device=dev, priority=-1)
         self.copy_impl = copy_impl
         self.timing = timing
-        self.op_granular = op_granular and copy_impl == "kernel"
+        self._op_granular_wanted = op_granular and copy_impl == "kernel"
+        self.op_granular = self._op_granular_wanted
         # Swap-ins also publish one flag per plane (layer), moved plane-major,
         # so compute can join a resumed request layer by layer (wait_plane).
+        self._layered_wanted = layered_swap_in
         self.layered_swap_in = layered_swap_in and self.op_granular
         self.num_planes = dataplane.geometry.num_planes
         self.pending: list[TransferRecord] = []
@@ -294,12 +298,18 @@ class StreamExecutor:
         if policy not in DUPLEX_POLICIES:
             raise ValueError(f"duplex policy must be one of {sorted(DUPLEX_POLICIES)}")
         pol = DUPLEX_POLICIES[policy]
+        path = pol.get("path", "lsu")
         for direction in ("out", "in"):
             ctas, threads, pace = pol[direction]
+            self.dp.set_path(direction, path)
             self.dp.set_launch(direction, ctas, threads)
             self.dp.set_pace(direction, pace)
         self.dp.set_budget(pol["budget"])
         self.dp.set_budget_priority(pol.get("priority"))
+        # The TMA bulk kernel signals whole plans only: per-op / per-plane
+        # waits need the LSU kernel, so a bulk policy waits per plan.
+        self.op_granular = self._op_granular_wanted and path == "lsu"
+        self.layered_swap_in = self._layered_wanted and self.op_granular
         self.duplex_policy = policy
 
     def _prune(self) -> None:

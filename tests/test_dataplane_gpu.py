@@ -557,3 +557,36 @@ def test_split_kv_layout_vs_oracle(cuda_ok):
     orc.apply_plan("in", back, want, ops)
     np.testing.assert_array_equal(cache.planes.cpu().numpy(), back)
     host.close()
+
+
+def test_executor_throughput_policy_bulk_round_trip(cuda_ok):
+    """The throughput policy runs both directions on the TMA bulk kernel with
+    plan-level waits: a swap-in reading host blocks a queued swap-out writes
+    (RAW across streams) still sees the swapped-out bytes."""
+    torch = cuda_ok
+    from paper_2411_18424_b200.cpu_store import TransferOp
+    from paper_2411_18424_b200.swap import StreamExecutor
+
+    geo = _small_geometry(1028, 4)
+    cache, host, dp = _mk(torch, geo, 1024, 1024)
+    ex = StreamExecutor(dp, duplex_policy="throughput")
+    assert not ex.op_granular
+    pattern = orc.kv_pattern(29, geo.num_planes, 1024, geo.plane_chunk_bytes)
+    cache.planes.copy_(torch.from_numpy(pattern))
+    torch.cuda.synchronize()
+    out_ops = [TransferOp(40, 40 * i, 100 + 40 * i) for i in range(8)]
+    in_ops = [TransferOp(40, 600 + 40 * i, 100 + 40 * i) for i in range(8)]
+    l0 = dp.launches
+    ex.submit("out", out_ops)
+    rec = ex.submit("in", in_ops)  # must wait for the out plan (RAW on host blocks)
+    assert rec.deps == 1 and ex.plan_waits == 1
+    ex.synchronize()
+    assert dp.launches - l0 == 2
+    want = pattern.copy()
+    host_img = np.zeros((1024, geo.block_bytes), np.uint8)
+    orc.apply_plan("out", pattern, host_img, [(o.blocks, o.gpu_start, o.cpu_start) for o in out_ops])
+    orc.apply_plan("in", want, host_img, [(o.blocks, o.gpu_start, o.cpu_start) for o in in_ops])
+    np.testing.assert_array_equal(cache.planes.cpu().numpy(), want)
+    ex.set_duplex_policy("latency")
+    assert ex.op_granular
+    host.close()

@@ -34,9 +34,12 @@ def test_adjacent_extents_do_not_conflict():
 
 def test_duplex_policies_are_well_formed():
     for name, pol in DUPLEX_POLICIES.items():
+        path = pol.get("path", "lsu")
+        assert path in ("lsu", "bulk"), name
         for d in ("out", "in"):
             ctas, threads, pace = pol[d]
-            assert ctas >= 1 and threads % 32 == 0 and 32 <= threads <= 1024, name
+            assert ctas >= 1 and threads % 32 == 0, name
+            assert (32 <= threads <= 1024) if path == "lsu" else threads == 0, name
             assert pace >= 0.0
         assert pol["budget"] >= 0.0
     # serving: swap-out paced below the link, swap-in bounded by reads in flight
