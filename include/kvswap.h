@@ -101,7 +101,10 @@ int kvs_destroy(KvsHandle* h);
 int kvs_set_launch(KvsHandle* h, int dir, int ctas, int threads);
 
 /* Select the kernel path for one direction.  piece_bytes / stages tune the
- * bulk path's smem ring (0 = defaults: 16 KiB x 4); ignored by the LSU path. */
+ * bulk path's smem ring (0 = defaults: 16 KiB x 4); ignored by the LSU path.
+ * The bulk path serves kvs_swap (whole-plan done flag); kvs_swap_ops,
+ * kvs_swap_layered and kvs_swap_signaled always run the LSU kernel, whose
+ * warps credit per-op / per-plane counters. */
 int kvs_set_path(KvsHandle* h, int dir, int path, int piece_bytes, int stages);
 
 /* Pace one direction's LSU kernel to `gbps` GB/s (0 = unpaced).  Stores to
