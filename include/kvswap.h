@@ -147,6 +147,12 @@ int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
 int kvs_swap_layered(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
                      uint64_t stream, uint32_t* plane_flags, uint32_t seq);
 
+/* Plane-major order granularity of kvs_swap_layered / plane-flagged
+ * kvs_swap_signaled: planes are moved in groups of `planes` (block-major
+ * inside a group), 0 = auto (>= 256 KiB of a block per group, so host reads
+ * stay long).  Plane l's flag still fires once plane l landed. */
+int kvs_set_layer_group(KvsHandle* h, int planes);
+
 /* Op-granular completion (SURVEY §7 hard part 4): same bytes as kvs_swap;
  * op_flags[i] (device or mapped, n_ops words) receives `seq` with
  * system-scope release once TransferOp i has fully landed, and done_flag

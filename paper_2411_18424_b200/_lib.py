@@ -51,6 +51,7 @@ EXPORTED_SYMBOLS = (
     "kvs_set_budget_priority",
     "kvs_swap",
     "kvs_swap_layered",
+    "kvs_set_layer_group",
     "kvs_swap_ops",
     "kvs_swap_signaled",
     "kvs_wait_flag",
@@ -119,6 +120,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_set_budget.argtypes = [c.c_void_p, c.c_double]
     lib.kvs_set_budget_priority.restype = c.c_int
     lib.kvs_set_budget_priority.argtypes = [c.c_void_p, c.c_int]
+    lib.kvs_set_layer_group.restype = c.c_int
+    lib.kvs_set_layer_group.argtypes = [c.c_void_p, c.c_int]
     lib.kvs_swap.restype = c.c_int
     lib.kvs_swap.argtypes = [
         c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_uint64, c.c_void_p, c.c_uint32,

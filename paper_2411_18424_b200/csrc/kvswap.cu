@@ -63,8 +63,8 @@ struct SwapParams {
   uint32_t stages;             // bulk path: smem ring depth
   uint32_t layered;            // 1: plane-major order + per-plane completion flags
   uint32_t pieces_per_plane;   // blocks * pieces_per_chunk
-  unsigned long long* plane_ctr;   // [num_planes] monotone piece counters (this direction)
-  unsigned long long plane_base;   // counter value before this launch
+  uint32_t layer_group;        // layered order: planes per group (>= 1)
+  unsigned long long* plane_ctr;   // [plane groups] piece counters, zeroed before the launch
   uint32_t* plane_flags;       // [num_planes]: receives seq when a plane has landed
   uint32_t* op_ctr;            // [n_ops] piece counters, zeroed before the launch
   uint32_t* op_flags;          // [n_ops]: receives seq when a TransferOp has landed
@@ -111,17 +111,24 @@ __device__ __forceinline__ void publish(uint32_t* flag, uint32_t seq) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
 }
 
-// Add a warp's `n` finished pieces of `plane` to the plane's counter; the
-// warp that completes the plane publishes seq.  Warp-uniform call.
+// Add a warp's `n` finished pieces of plane group `grp` to the group's
+// counter; the warp that completes the group publishes seq for every plane
+// of it.  Warp-uniform call.
 template <int CAP>
-__device__ __forceinline__ void credit_plane(const SwapParams<CAP>& p, uint32_t lane,
-                                             uint32_t plane, uint32_t n) {
+__device__ __forceinline__ void credit_group(const SwapParams<CAP>& p, uint32_t lane,
+                                             uint32_t grp, uint32_t n) {
   if (p.plane_flags == nullptr || n == 0) return;
   __syncwarp();  // every lane's stores precede lane 0's fence
   if (lane == 0) {
     __threadfence_system();
-    const unsigned long long old = atomicAdd(p.plane_ctr + plane, static_cast<unsigned long long>(n));
-    if (old + n == p.plane_base + p.pieces_per_plane) publish(p.plane_flags + plane, p.seq);
+    const uint32_t first = grp * p.layer_group;
+    const uint32_t g_here = min(p.layer_group, p.num_planes - first);
+    const unsigned long long want =
+        static_cast<unsigned long long>(p.pieces_per_plane) * g_here;
+    const unsigned long long old =
+        atomicAdd(p.plane_ctr + grp, static_cast<unsigned long long>(n));
+    if (old + n == want)
+      for (uint32_t l = 0; l < g_here; ++l) publish(p.plane_flags + first + l, p.seq);
   }
 }
 
@@ -149,20 +156,29 @@ __global__ void __launch_bounds__(kMaxThreads)
   int op = 0;
   int32_t op_begin = 0;
   const uint64_t t0 = p.pace_ps != 0 ? globaltimer_ns() : 0;
-  const bool tracking = p.plane_flags != nullptr || p.op_flags != nullptr;
-  uint32_t acc_plane = 0xFFFFFFFFu, acc_plane_n = 0;  // uncredited pieces of acc_plane
+  const bool ops_at_end = p.layered && p.op_flags != nullptr;
+  const bool op_per_warp = p.op_flags != nullptr && !ops_at_end;
+  const bool tracking = p.plane_flags != nullptr || op_per_warp;
+  uint32_t acc_grp = 0xFFFFFFFFu, acc_grp_n = 0;  // uncredited pieces of plane group acc_grp
   int acc_op = -1;
   uint32_t acc_op_n = 0, acc_op_want = 0;  // uncredited pieces of acc_op, its total
   for (uint32_t i = warp; i < p.total_pieces; i += nwarps) {
     uint32_t k, plane, piece;
     if (p.layered) {
-      // Plane-major: every block of plane 0, then plane 1, ... so layer l's
-      // KV lands (and is flagged) before layer l+1's.
-      plane = i / p.pieces_per_plane;
-      const uint32_t j = i - plane * p.pieces_per_plane;
-      k = j / p.pieces_per_chunk;
-      piece = j - k * p.pieces_per_chunk;
-      if (static_cast<int32_t>(k) < op_begin) {  // next plane: rewind the cursor
+      // Plane-major in groups of layer_group planes: every block of planes
+      // [0, g), then of [g, 2g), ... so layer l's KV lands (and is flagged)
+      // before later groups'.  Within a group the order
+      // is block-major, so the host side still reads g x chunk contiguous.
+      const uint32_t g = p.layer_group;
+      const uint32_t per_group = p.pieces_per_plane * g;
+      const uint32_t group = i / per_group;
+      const uint32_t j = i - group * per_group;
+      const uint32_t g_here = min(g, p.num_planes - group * g);
+      const uint32_t chunk_idx = j / p.pieces_per_chunk;
+      piece = j - chunk_idx * p.pieces_per_chunk;
+      k = chunk_idx / g_here;
+      plane = group * g + (chunk_idx - k * g_here);
+      if (static_cast<int32_t>(k) < op_begin) {  // next group: rewind the cursor
         op = 0;
         op_begin = 0;
       }
@@ -225,38 +241,44 @@ __global__ void __launch_bounds__(kMaxThreads)
       // Credit finished pieces lazily: only when this warp moves to another
       // plane / op (or exits) does it fence and add its count, so the system
       // fences scale with (warps x planes), not with pieces.
-      if (p.plane_flags != nullptr && plane != acc_plane) {
-        credit_plane(p, lane, acc_plane, acc_plane_n);
-        acc_plane = plane;
-        acc_plane_n = 0;
+      if (p.plane_flags != nullptr && plane / p.layer_group != acc_grp) {
+        credit_group(p, lane, acc_grp, acc_grp_n);
+        acc_grp = plane / p.layer_group;
+        acc_grp_n = 0;
       }
-      if (p.op_flags != nullptr && op != acc_op) {
+      if (op_per_warp && op != acc_op) {
         credit_op(p, lane, acc_op, acc_op_n, acc_op_want);
         acc_op = op;
         acc_op_n = 0;
         acc_op_want = static_cast<uint32_t>(p.op_end[op] - op_begin) * p.num_planes *
                       p.pieces_per_chunk;
       }
-      ++acc_plane_n;
+      ++acc_grp_n;
       ++acc_op_n;
     }
   }
   if (tracking) {
-    credit_plane(p, lane, acc_plane, acc_plane_n);
-    credit_op(p, lane, acc_op, acc_op_n, acc_op_want);
+    credit_group(p, lane, acc_grp, acc_grp_n);
+    if (op_per_warp) credit_op(p, lane, acc_op, acc_op_n, acc_op_want);
   }
 
-  if (p.done_flag != nullptr) {
+  if (p.done_flag != nullptr || ops_at_end) {
     // Last CTA to retire publishes `seq` with system-scope release, after
-    // every CTA fenced its stores (host-visible for swap-out).
+    // every CTA fenced its stores (host-visible for swap-out).  In plane-major
+    // order a TransferOp is complete only once its last plane is, i.e. at
+    // the very end, so its op flags are published here too instead of being
+    // counted per warp (which would fence at every op change of every plane).
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence_system();
       const unsigned long long t = atomicAdd(p.ticket, 1ull);
       if (t == p.ticket_base + gridDim.x - 1) {
         __threadfence_system();
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.seq)
-                     : "memory");
+        if (ops_at_end)
+          for (int32_t i = 0; i < p.n_ops; ++i) publish(p.op_flags + i, p.seq);
+        if (p.done_flag != nullptr)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.seq)
+                       : "memory");
       }
     }
   }
@@ -441,12 +463,12 @@ struct KvsHandle {
   int path[2] = {KVS_PATH_LSU, KVS_PATH_LSU};
   unsigned long long* d_plane_ctr = nullptr;    // [2][num_planes]
   uint32_t* d_op_ctr = nullptr;                 // [2][kOpsPerLaunchMax]
-  unsigned long long plane_next[2] = {0, 0};
   int piece_bytes[2] = {0, 0};
   int stages[2] = {0, 0};
   uint64_t pace_ps[2] = {0, 0};  // per 4 KiB piece; 0 = unpaced
   double budget_gbps = 0.0;      // shared by both directions; 0 = none
   int budget_priority = -1;      // direction that charges the budget without waiting
+  int layer_group = 0;           // layered order: planes per group (0 = auto)
   unsigned long long* d_bucket = nullptr;
   int64_t launches = 0;
 };
@@ -464,6 +486,7 @@ constexpr int kDefaultThreads = 512;
 constexpr int kDefaultBulkPiece = 16384;
 constexpr int kDefaultStages = 4;
 constexpr int kDefaultBulkCtas = 64;
+constexpr int64_t kLayerGroupBytes = 256 * 1024;
 
 // Validate ops against both pools; fill op tables.  Returns KVS_OK or error.
 int check_ops(const KvsHandle* h, const int32_t* ops, int32_t n_ops, int64_t* total_blocks) {
@@ -524,10 +547,25 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   }
   p.layered = o.layered ? 1u : 0u;
   p.pieces_per_plane = static_cast<uint32_t>(blocks) * p.pieces_per_chunk;
+  {
+    // Auto: enough planes per group that a block's group is >= 256 KiB of
+    // contiguous host memory (strict plane-major reads 64 KiB every 2 MiB).
+    int64_t g = h->layer_group > 0 ? h->layer_group
+                                   : (kLayerGroupBytes + h->geo.plane_chunk_bytes - 1) /
+                                         h->geo.plane_chunk_bytes;
+    if (g < 1) g = 1;
+    if (g > h->geo.num_planes) g = h->geo.num_planes;
+    p.layer_group = static_cast<uint32_t>(g);
+  }
   p.plane_ctr = h->d_plane_ctr + static_cast<size_t>(dir) * h->geo.num_planes;
-  p.plane_base = h->plane_next[dir];
   p.plane_flags = o.plane_flags;
-  if (o.plane_flags != nullptr) h->plane_next[dir] += p.pieces_per_plane;
+  if (o.plane_flags != nullptr) {
+    // Same stream as the kernel: ordered after the previous launch of this
+    // direction that used the group counters.
+    const uint32_t groups = (p.num_planes + p.layer_group - 1) / p.layer_group;
+    int rc = cuda_rc(cudaMemsetAsync(p.plane_ctr, 0, sizeof(unsigned long long) * groups, stream));
+    if (rc) return rc;
+  }
   p.op_ctr = h->d_op_ctr + static_cast<size_t>(dir) * kOpsPerLaunchMax;
   p.op_flags = o.op_flags;
   // pace_ps is per 4 KiB; the bulk path paces per (larger) TMA piece.
@@ -538,7 +576,8 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   if (p.bucket_cost_ns == 0 && h->budget_gbps > 0.0) p.bucket_cost_ns = 1;
   p.bucket_burst_ns = 16 * p.bucket_cost_ns;
   p.bucket_nowait = h->budget_priority == dir ? 1u : 0u;
-  if (o.op_flags != nullptr) {
+  const bool ops_at_end = o.layered && o.op_flags != nullptr;
+  if (o.op_flags != nullptr && !ops_at_end) {
     // Same stream as the kernel: ordered before it, and after the previous
     // launch of this direction that used the counters.
     int rc = cuda_rc(cudaMemsetAsync(p.op_ctr, 0, sizeof(uint32_t) * n_ops, stream));
@@ -555,7 +594,8 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   p.ticket = h->d_tickets + dir;
   p.ticket_base = h->ticket_next[dir];
   p.seq = o.seq;
-  if (o.done_flag != nullptr) h->ticket_next[dir] += static_cast<unsigned long long>(ctas);
+  if (o.done_flag != nullptr || ops_at_end)
+    h->ticket_next[dir] += static_cast<unsigned long long>(ctas);
   if (bulk) {
     const size_t smem = static_cast<size_t>(stages) * static_cast<size_t>(piece);
     auto kern = dir == KVS_DIR_OUT ? kvs_swap_bulk_kernel<KVS_DIR_OUT, CAP>
@@ -706,6 +746,12 @@ int kvs_set_budget_priority(KvsHandle* h, int dir) {
   if (h == nullptr || (dir != -1 && dir != KVS_DIR_OUT && dir != KVS_DIR_IN))
     return KVS_ERR_INVALID;
   h->budget_priority = dir;
+  return KVS_OK;
+}
+
+int kvs_set_layer_group(KvsHandle* h, int planes) {
+  if (h == nullptr || planes < 0) return KVS_ERR_INVALID;
+  h->layer_group = planes;
   return KVS_OK;
 }
 

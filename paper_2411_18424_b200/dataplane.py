@@ -230,6 +230,10 @@ class SwapDataPlane:
         """One GB/s budget shared by swap-out and swap-in (0 = none)."""
         _lib.check(self.lib.kvs_set_budget(self.handle, float(gbps)), "kvs_set_budget")
 
+    def set_layer_group(self, planes: int = 0) -> None:
+        """Planes per group in plane-major (layered) order; 0 = auto."""
+        _lib.check(self.lib.kvs_set_layer_group(self.handle, planes), "kvs_set_layer_group")
+
     def set_budget_priority(self, direction: Optional[str]) -> None:
         """Direction that charges the shared budget without waiting (None = neither)."""
         d = -1 if direction is None else _lib.DIRECTIONS[direction]

@@ -228,14 +228,17 @@ def test_config1_round_trip_llama3_8b(cuda_ok, path):
     host.close()
 
 
+@pytest.mark.parametrize("group", [0, 1, 4])
 @pytest.mark.parametrize("direction", ["in", "out"])
-def test_layered_swap_flags_each_plane(cuda_ok, direction):
-    """kvs_swap_layered: plane-major order, per-plane release flags; a consumer
-    stream waiting on plane l's flag sees plane l's bytes complete."""
+def test_layered_swap_flags_each_plane(cuda_ok, direction, group):
+    """kvs_swap_layered: plane-major order (in groups of `group` planes, 0 =
+    auto; 6 planes / 4 leaves a partial last group), per-plane release flags;
+    a consumer stream waiting on plane l's flag sees plane l's bytes complete."""
     torch = cuda_ok
     geo = _small_geometry(1028, 6)
     G = C = 600
     cache, host, dp = _mk(torch, geo, G, C, ctas={"out": 4, "in": 4})
+    dp.set_layer_group(group)
     rng = np.random.default_rng(21)
     pattern = orc.kv_pattern(3, geo.num_planes, G, geo.plane_chunk_bytes)
     gpu_tab = orc.random_block_table(rng, 500, G)
