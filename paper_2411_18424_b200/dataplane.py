@@ -18,7 +18,7 @@ Reference seam: kvswitch models a swap as timestamps only
 from __future__ import annotations
 
 import ctypes
-from typing import Iterable, Optional, Sequence, Union
+from typing import Optional, Sequence, Union
 
 import numpy as np
 import torch

@@ -36,8 +36,8 @@ import torch
 from . import _lib
 from .costmodel import TransferParams, iteration_time
 from .core import elapsed
-from .engine import (EFFICIENCY_INTERVAL_ITERS, Engine, EngineConfig, IterationRecord,
-                     MetricsReport, percentile)
+from .engine import (EFFICIENCY_INTERVAL_ITERS, RUNNING, SWAPPING_IN, Engine, EngineConfig,
+                     IterationRecord, MetricsReport, percentile)
 from .swap import decide_mode
 
 LIVE_DEADLOCK_ITERATIONS = 200_000
@@ -243,11 +243,10 @@ class LiveEngine(Engine):
             return super()._mark_running(req)
         # Joining layer by layer: running now, bytes checked once decode has
         # waited for every layer (verification needs the whole KV).
-        from .engine import SWAPPING_IN
         st = self.states.get(req)
         if st is None or st.phase != SWAPPING_IN:
             return False
-        st.phase = "running"
+        st.phase = RUNNING
         self.qs.move(req, "running")
         self._mark_turn(req, 2)
         self._deferred.append(req)
