@@ -127,8 +127,12 @@ __device__ __forceinline__ void credit_group(const SwapParams<CAP>& p, uint32_t 
         static_cast<unsigned long long>(p.pieces_per_plane) * g_here;
     const unsigned long long old =
         atomicAdd(p.plane_ctr + grp, static_cast<unsigned long long>(n));
-    if (old + n == want)
+    if (old + n == want) {
+      // Every piece of the group is counted: publish, and leave the counter
+      // at zero for the next launch of this direction (no memset node).
+      p.plane_ctr[grp] = 0;
       for (uint32_t l = 0; l < g_here; ++l) publish(p.plane_flags + first + l, p.seq);
+    }
   }
 }
 
@@ -140,7 +144,10 @@ __device__ __forceinline__ void credit_op(const SwapParams<CAP>& p, uint32_t lan
   __syncwarp();
   if (lane == 0) {
     __threadfence_system();
-    if (atomicAdd(p.op_ctr + op, n) + n == want) publish(p.op_flags + op, p.seq);
+    if (atomicAdd(p.op_ctr + op, n) + n == want) {
+      p.op_ctr[op] = 0;  // counted in full: reset for the next launch
+      publish(p.op_flags + op, p.seq);
+    }
   }
 }
 
@@ -559,13 +566,6 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   }
   p.plane_ctr = h->d_plane_ctr + static_cast<size_t>(dir) * h->geo.num_planes;
   p.plane_flags = o.plane_flags;
-  if (o.plane_flags != nullptr) {
-    // Same stream as the kernel: ordered after the previous launch of this
-    // direction that used the group counters.
-    const uint32_t groups = (p.num_planes + p.layer_group - 1) / p.layer_group;
-    int rc = cuda_rc(cudaMemsetAsync(p.plane_ctr, 0, sizeof(unsigned long long) * groups, stream));
-    if (rc) return rc;
-  }
   p.op_ctr = h->d_op_ctr + static_cast<size_t>(dir) * kOpsPerLaunchMax;
   p.op_flags = o.op_flags;
   // pace_ps is per 4 KiB; the bulk path paces per (larger) TMA piece.
@@ -576,13 +576,9 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   if (p.bucket_cost_ns == 0 && h->budget_gbps > 0.0) p.bucket_cost_ns = 1;
   p.bucket_burst_ns = 16 * p.bucket_cost_ns;
   p.bucket_nowait = h->budget_priority == dir ? 1u : 0u;
-  const bool ops_at_end = o.layered && o.op_flags != nullptr;
-  if (o.op_flags != nullptr && !ops_at_end) {
-    // Same stream as the kernel: ordered before it, and after the previous
-    // launch of this direction that used the counters.
-    int rc = cuda_rc(cudaMemsetAsync(p.op_ctr, 0, sizeof(uint32_t) * n_ops, stream));
-    if (rc) return rc;
-  }
+  // Op / plane-group counters: zero at create; the warp that completes an op
+  // (group) resets its counter, so the next launch of this direction (same
+  // stream) starts from zero without a memset node.
   int threads = bulk ? 32 : (h->threads[dir] > 0 ? h->threads[dir] : kDefaultThreads);
   int ctas = h->ctas[dir] > 0 ? h->ctas[dir] : (bulk ? kDefaultBulkCtas : default_ctas(dir));
   // Never launch warps (bulk: CTAs) that can have no piece.
@@ -594,7 +590,7 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   p.ticket = h->d_tickets + dir;
   p.ticket_base = h->ticket_next[dir];
   p.seq = o.seq;
-  if (o.done_flag != nullptr || ops_at_end)
+  if (o.done_flag != nullptr || (!bulk && o.layered && o.op_flags != nullptr))
     h->ticket_next[dir] += static_cast<unsigned long long>(ctas);
   if (bulk) {
     const size_t smem = static_cast<size_t>(stages) * static_cast<size_t>(piece);
@@ -697,6 +693,7 @@ int kvs_create(int device, const KvsGeometry* geo, const uint64_t* plane_ptrs, v
     rc = cuda_rc(
         cudaMemset(h->d_plane_ctr, 0, 2 * sizeof(unsigned long long) * geo->num_planes));
   if (!rc) rc = cuda_rc(cudaMalloc(&h->d_op_ctr, 2 * sizeof(uint32_t) * kOpsPerLaunchMax));
+  if (!rc) rc = cuda_rc(cudaMemset(h->d_op_ctr, 0, 2 * sizeof(uint32_t) * kOpsPerLaunchMax));
   if (!rc) rc = cuda_rc(cudaMalloc(&h->d_bucket, sizeof(unsigned long long)));
   if (!rc) rc = cuda_rc(cudaMemset(h->d_bucket, 0, sizeof(unsigned long long)));
   if (rc) {
