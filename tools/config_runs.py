@@ -9,7 +9,8 @@ the identical plan stream over its own PCIe link).
 
 python tools/config_runs.py c3 c4 c5   -> gpurun_out/config_runs.json
 (SM_PARTITION=8 by default: live runs put the swap kernels on their own 8-SM
-green context and decode on the rest; SM_PARTITION=0 shares all SMs.)
+green context and decode on the rest; SM_PARTITION=0 shares all SMs.
+LAYERED=1 by default: FastSwitch runs with layered admission.)
 """
 
 import dataclasses
@@ -33,6 +34,7 @@ from paper_2411_18424_b200.workload import generate  # noqa: E402
 
 
 SM_PARTITION = int(os.environ.get("SM_PARTITION", "8"))
+LAYERED = os.environ.get("LAYERED", "1") == "1"  # FastSwitch runs with layered admission
 
 
 def swap_rates(rt):
@@ -50,9 +52,10 @@ def swap_rates(rt):
 def live_run(geo, doc, impl="kernel", decode=None, verify=False):
     cfg, wl, _ = mconfig.build(doc)
     cfg = dataclasses.replace(cfg, transfer=b200_transfer_params())
+    layered = LAYERED and impl == "kernel"
     rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, copy_impl=impl,
-                 verify=verify, timing=True, sm_partition=SM_PARTITION)
-    eng = LiveEngine(cfg, generate(wl), rt, decode)
+                 verify=verify, timing=True, sm_partition=SM_PARTITION, layered_swap_in=layered)
+    eng = LiveEngine(cfg, generate(wl), rt, decode, layered=layered)
     eng.turn_trace = []
     t0 = time.perf_counter()
     rep = eng.run()
