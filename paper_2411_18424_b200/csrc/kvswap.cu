@@ -1141,38 +1141,48 @@ __global__ void __launch_bounds__(256) kvs_kv_tokens_kernel(const __grid_constan
   const uint32_t total_tokens = static_cast<uint32_t>(s.seg_tok_end[s.n_segs - 1]);
   const uint64_t rows = static_cast<uint64_t>(total_tokens) * s.n_planes * 2u;
   const bool vec = (s.words & 3u) == 0;
+  // Units per row (16 B vectors, or words); short rows (TP shards: 256 B)
+  // share a warp, so every lane has a unit whatever the head count.
+  const uint32_t upr = vec ? s.words / 4 : s.words;
+  const uint32_t rpw = upr >= 32 ? 1u : 32u / upr;  // rows per warp
+  const uint32_t sub = upr >= 32 ? 0u : lane / upr;
+  const uint32_t w0 = upr >= 32 ? lane : lane % upr;
+  const uint32_t wstep = upr >= 32 ? 32u : upr;
   uint32_t bad = 0;
   uint32_t seg = 0;
-  for (uint64_t r = warp; r < rows; r += nwarps) {
-    const uint32_t kv = static_cast<uint32_t>(r & 1u);
-    const uint64_t rp = r >> 1;
-    const uint32_t plane = s.plane_lo + static_cast<uint32_t>(rp % s.n_planes);
-    const uint32_t i = static_cast<uint32_t>(rp / s.n_planes);  // flat token index
-    while (static_cast<int32_t>(i) >= s.seg_tok_end[seg]) ++seg;
-    const int32_t seg_begin = seg == 0 ? 0 : s.seg_tok_end[seg - 1];
-    const uint32_t tok = static_cast<uint32_t>(s.seg_lo[seg] + (static_cast<int32_t>(i) - seg_begin));
-    const uint32_t blk = s.seg_phys[seg] + tok / s.block_tokens -
-                         static_cast<uint32_t>(s.seg_lo[seg]) / s.block_tokens;
-    const uint32_t slot = tok % s.block_tokens;
-    uint32_t* row = reinterpret_cast<uint32_t*>(
-        reinterpret_cast<char*>(__ldg(s.planes + plane)) + static_cast<int64_t>(blk) * s.stride) +
-        (static_cast<uint64_t>(kv) * s.block_tokens + slot) * s.words;
-    const uint32_t base = kv_word(s.seg_req[seg], tok, plane, kv, 0);
-    if (vec) {
-      uint4* row4 = reinterpret_cast<uint4*>(row);
-      for (uint32_t w = lane; w < s.words / 4; w += 32) {
-        const uint32_t b0 = base + 4 * w;
-        if (s.mode == 0) {
-          row4[w] = make_uint4(b0, b0 + 1, b0 + 2, b0 + 3);
-        } else {
-          const uint4 v = row4[w];
-          bad += (v.x != b0) + (v.y != b0 + 1) + (v.z != b0 + 2) + (v.w != b0 + 3);
+  if (sub < rpw) {
+    for (uint64_t r = warp * rpw + sub; r < rows; r += nwarps * rpw) {
+      const uint32_t kv = static_cast<uint32_t>(r & 1u);
+      const uint64_t rp = r >> 1;
+      const uint32_t plane = s.plane_lo + static_cast<uint32_t>(rp % s.n_planes);
+      const uint32_t i = static_cast<uint32_t>(rp / s.n_planes);  // flat token index
+      while (static_cast<int32_t>(i) >= s.seg_tok_end[seg]) ++seg;
+      const int32_t seg_begin = seg == 0 ? 0 : s.seg_tok_end[seg - 1];
+      const uint32_t tok =
+          static_cast<uint32_t>(s.seg_lo[seg] + (static_cast<int32_t>(i) - seg_begin));
+      const uint32_t blk = s.seg_phys[seg] + tok / s.block_tokens -
+                           static_cast<uint32_t>(s.seg_lo[seg]) / s.block_tokens;
+      const uint32_t slot = tok % s.block_tokens;
+      uint32_t* row = reinterpret_cast<uint32_t*>(
+          reinterpret_cast<char*>(__ldg(s.planes + plane)) + static_cast<int64_t>(blk) * s.stride) +
+          (static_cast<uint64_t>(kv) * s.block_tokens + slot) * s.words;
+      const uint32_t base = kv_word(s.seg_req[seg], tok, plane, kv, 0);
+      if (vec) {
+        uint4* row4 = reinterpret_cast<uint4*>(row);
+        for (uint32_t w = w0; w < upr; w += wstep) {
+          const uint32_t b0 = base + 4 * w;
+          if (s.mode == 0) {
+            row4[w] = make_uint4(b0, b0 + 1, b0 + 2, b0 + 3);
+          } else {
+            const uint4 v = row4[w];
+            bad += (v.x != b0) + (v.y != b0 + 1) + (v.z != b0 + 2) + (v.w != b0 + 3);
+          }
         }
+      } else if (s.mode == 0) {
+        for (uint32_t w = w0; w < upr; w += wstep) row[w] = base + w;
+      } else {
+        for (uint32_t w = w0; w < upr; w += wstep) bad += row[w] != base + w;
       }
-    } else if (s.mode == 0) {
-      for (uint32_t w = lane; w < s.words; w += 32) row[w] = base + w;
-    } else {
-      for (uint32_t w = lane; w < s.words; w += 32) bad += row[w] != base + w;
     }
   }
   if (s.mode == 1) {
@@ -1227,7 +1237,9 @@ extern "C" int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_
     if (n == 0) continue;
     s.n_segs = n;
     const uint64_t rows = static_cast<uint64_t>(tokens) * s.n_planes * 2;
-    const uint64_t want = (rows + 7) / 8;  // 8 warps per CTA
+    const uint32_t upr = (s.words & 3u) == 0 ? s.words / 4 : s.words;
+    const uint64_t rows_per_cta = 8ull * (upr >= 32 ? 1u : 32u / upr);  // 8 warps per CTA
+    const uint64_t want = (rows + rows_per_cta - 1) / rows_per_cta;
     const int ctas = static_cast<int>(want < 1184 ? want : 1184);
     kvs_kv_tokens_kernel<<<ctas, 256, 0, st>>>(s);
     rc = cuda_rc(cudaGetLastError());

@@ -125,7 +125,7 @@ def test_live_engine_bytes_and_latency(cuda_ok):
     rt.close()
 
 
-@pytest.mark.parametrize("geo_name", ["tiny", "llama3-8b"])
+@pytest.mark.parametrize("geo_name", ["tiny", "llama3-8b", "llama3-70b-tp8"])
 def test_kv_token_kernel_matches_torch_pattern(cuda_ok, geo_name):
     """kvs_kv_tokens (write + check) against the plain torch restatement."""
     import numpy as np
@@ -134,7 +134,8 @@ def test_kv_token_kernel_matches_torch_pattern(cuda_ok, geo_name):
     from paper_2411_18424_b200.geometry import PRESETS
     from paper_2411_18424_b200.runtime import Runtime, token_segments
 
-    geo = TINY if geo_name == "tiny" else PRESETS[geo_name]
+    geo = (TINY if geo_name == "tiny" else PRESETS["llama3-70b"].with_tp(8)
+           if geo_name == "llama3-70b-tp8" else PRESETS[geo_name])
     G = 64
     rt = Runtime(geo, G, 8, verify=True)
     rt.cache.planes.fill_(0)
