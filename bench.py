@@ -236,7 +236,7 @@ def run_ours(args, geo):
     import torch.distributed as dist
 
     from paper_2411_18424_b200.dataplane import (HostKVPool, PagedKVCache, SwapDataPlane,
-                                                 numa_nodes)
+                                                 host_link_info, numa_nodes)
 
     rank, world, local = dist_env()
     if not torch.cuda.is_available():
@@ -350,9 +350,16 @@ def run_ours(args, geo):
                "sample": sample, "cpu_model": cpu_model()}
 
     numa_per_rank = [host_numa]
-    if world > 1:  # where each rank's swap space lives (NUMA node of its GPU)
+    links = [host_link_info(dev)]
+    if world > 1:  # where each rank's swap space lives, and which host link it uses
         numa_per_rank = [None] * world
         dist.all_gather_object(numa_per_rank, host_numa)
+        links = [None] * world
+        dist.all_gather_object(links, host_link_info(dev))
+    root_ports = {l["root_port"] for l in links if l.get("root_port")}
+    # Ranks behind one root port share its link: the aggregate roofline is the
+    # smaller of one link per rank and one per distinct root port.
+    link_cap = PCIE_GEN5_X16_GBS * (min(world, len(root_ports)) if root_ports else world)
     if rank == 0:
         dominant, dom_ms = ("in", in_ms) if sum(in_ms) >= sum(out_ms) else ("out", out_ms)
         achieved = nbytes_dir / (statistics.mean(dom_ms) * 1e-3) / 1e9
@@ -378,7 +385,11 @@ def run_ours(args, geo):
                          "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
                          "frac": round(achieved / PCIE_GEN5_X16_GBS, 4), "traffic": traffic,
                          "aggregate": {"gbs": round(value, 3), "links": world,
-                                       "frac": round(value / (world * PCIE_GEN5_X16_GBS), 4)},
+                                       "frac": round(value / (world * PCIE_GEN5_X16_GBS), 4),
+                                       "root_ports": len(root_ports) or None,
+                                       "topology_cap_gbs": link_cap,
+                                       "frac_of_topology": round(value / link_cap, 4)},
+                         "host_links": links,
                          "kernel": f"kvs_swap_kernel<{dominant}>",
                          "peak_source": "PCIe Gen5 x16 per direction after 128b/130b "
                                         "(BASELINE.md §4; MEASURED_PEAKS.json has no PCIe entry)",

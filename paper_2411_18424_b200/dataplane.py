@@ -64,17 +64,79 @@ def numa_nodes() -> int:
     return max(1, n)
 
 
+def _gpu_bdf(device) -> Optional[str]:
+    try:
+        idx = torch.device(device if device is not None else "cuda").index
+        props = torch.cuda.get_device_properties(idx if idx is not None else 0)
+        return f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+    except (RuntimeError, AssertionError, ValueError):
+        return None
+
+
+def _smi_link(device) -> dict:
+    import subprocess
+
+    try:
+        idx = torch.device(device if device is not None else "cuda").index or 0
+        out = subprocess.run(
+            ["nvidia-smi", "-i", str(idx), "--format=csv,noheader,nounits",
+             "--query-gpu=pcie.link.gen.max,pcie.link.gen.gpumax,pcie.link.width.max"],
+            capture_output=True, text=True, timeout=10).stdout.strip()
+        gen, gpumax, width = [x.strip() for x in out.split(",")]
+        return {"link_speed": f"gen{gen} (device max gen{gpumax})", "link_width": width,
+                "source": "nvidia-smi"}
+    except (OSError, ValueError, subprocess.SubprocessError):
+        return {}
+
+
+def host_link_info(device=None) -> dict:
+    """The GPU's PCIe link as sysfs reports it (speed, width), its NUMA node,
+    and the root port it hangs off: GPUs behind one root port share that
+    port's host link, which caps their aggregate swap bandwidth."""
+    import os
+
+    bdf = _gpu_bdf(device)
+    info = {"bdf": bdf, "link_speed": None, "link_width": None, "max_link_speed": None,
+            "root_port": None, "numa_node": -1}
+    if bdf is None:
+        return info
+    base = f"/sys/bus/pci/devices/{bdf}"
+
+    def read(name):
+        try:
+            with open(f"{base}/{name}") as f:
+                return f.read().strip()
+        except OSError:
+            return None
+
+    info["link_speed"] = read("current_link_speed")
+    info["max_link_speed"] = read("max_link_speed")
+    info["link_width"] = read("current_link_width")
+    if info["link_speed"] is None:  # no PCI sysfs in this container: ask the driver
+        info.update(_smi_link(device))
+    node = read("numa_node")
+    info["numa_node"] = int(node) if node not in (None, "") else -1
+    try:
+        parts = os.path.realpath(base).split("/")
+        # /sys/devices/pci0000:00/<root port>/.../<gpu>: the first device below the host bridge
+        i = next(k for k, p in enumerate(parts) if p.startswith("pci"))
+        info["root_port"] = parts[i + 1] if len(parts) > i + 2 else None
+    except (StopIteration, OSError):
+        pass
+    return info
+
+
 def gpu_numa_node(device: Union[int, str, torch.device, None]) -> int:
     """NUMA node of the GPU's PCIe root (sysfs), or -1 when unknown.  Each
     rank's swap space belongs on its own GPU's socket: host-link traffic then
     never crosses the inter-socket fabric."""
+    bdf = _gpu_bdf(device)
+    if bdf is None:
+        return -1
     try:
-        idx = torch.device(device if device is not None else "cuda").index
-        props = torch.cuda.get_device_properties(idx if idx is not None else 0)
-        bdf = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
         with open(f"/sys/bus/pci/devices/{bdf}/numa_node") as f:
             return int(f.read().strip())
-    except (OSError, ValueError, RuntimeError, AssertionError):
+    except (OSError, ValueError):
         return -1
 
 
