@@ -593,3 +593,38 @@ def test_executor_throughput_policy_bulk_round_trip(cuda_ok):
     ex.set_duplex_policy("latency")
     assert ex.op_granular
     host.close()
+
+
+def test_kv_image_export_import_through_the_kernels(cuda_ok, tmp_path):
+    """Swap-out with the kernel into pinned host memory, export the request's
+    host image to a file, import it into another rank's pool at other host
+    blocks, swap it in with the kernel: byte-exact."""
+    torch = cuda_ok
+    from paper_2411_18424_b200.cpu_store import CpuStore
+    from paper_2411_18424_b200.geometry import LLAMA3_8B
+    from paper_2411_18424_b200.kvimage import export_image, import_image
+
+    geo = LLAMA3_8B.with_tp(4)  # 512 KiB blocks
+    G = C = 128
+    cache, host, dp = _mk(torch, geo, G, C)
+    cache.planes.view(torch.int32).random_(generator=torch.Generator(device="cuda:0").manual_seed(3))
+    torch.cuda.synchronize()
+    store = CpuStore(C)
+    gpu_ext = [(10, 20), (64, 13)]
+    plan = store.plan_swap_out(7, 33, gpu_ext)
+    dp.swap("out", plan.all_ops())
+    torch.cuda.synchronize()
+    path = str(tmp_path / "req7.kvimg")
+    export_image(store, host.array, 7, geo, path)
+
+    cache2, host2, dp2 = _mk(torch, geo, G, C)
+    store2 = CpuStore(C)
+    store2.plan_swap_out(1, 40, [(0, 40)])  # occupy the front of the second pool
+    import_image(path, store2, host2.array, 7, geo)
+    new_ext = [(90, 33)]
+    dp2.swap("in", store2.plan_swap_in(7, new_ext).all_ops())
+    torch.cuda.synchronize()
+    src = torch.cat([cache.planes[:, s:s + n] for s, n in gpu_ext], dim=1)
+    assert torch.equal(cache2.planes[:, 90:123], src)
+    host.close()
+    host2.close()

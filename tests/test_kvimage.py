@@ -1,0 +1,72 @@
+"""The exported host KV image (paper_2411_18424_b200.kvimage): a request
+swapped out on one store, exported, imported into another store at other
+host blocks, and swapped in to another GPU table comes back byte-exact; bad
+images are rejected.  Host-side only (numpy pools, oracle byte restatement)."""
+
+import io
+
+import numpy as np
+import pytest
+
+from oracle import bytes_oracle as orc
+from paper_2411_18424_b200.cpu_store import CpuStore
+from paper_2411_18424_b200.geometry import KVGeometry
+from paper_2411_18424_b200.kvimage import KVImageError, export_image, import_image
+
+GEO = KVGeometry("img", num_layers=3, num_kv_heads=2, head_dim=8)  # 1 KiB chunks
+
+
+def _table(extents):
+    return np.concatenate([np.arange(s, s + n) for s, n in extents])
+
+
+def test_export_import_round_trip_is_byte_exact():
+    G, C = 96, 128
+    planes = orc.kv_pattern(3, GEO.num_planes, G, GEO.plane_chunk_bytes)
+    store, pool = CpuStore(C), np.zeros((C, GEO.block_bytes), np.uint8)
+    gpu_ext = [(30, 12), (70, 9)]
+    plan = store.plan_swap_out(5, 21, gpu_ext, tokens=21 * 16 - 5)
+    orc.apply_plan("out", planes, pool, [(o.blocks, o.gpu_start, o.cpu_start)
+                                         for o in plan.all_ops()])
+    buf = io.BytesIO()
+    hdr = export_image(store, pool, 5, GEO, buf)
+    assert hdr["blocks"] == 21 and hdr["tokens"] == 21 * 16 - 5
+
+    # another rank: some host blocks already taken, so the image lands elsewhere
+    store2, pool2 = CpuStore(C), np.zeros((C, GEO.block_bytes), np.uint8)
+    store2.plan_swap_out(9, 17, [(0, 17)])
+    buf.seek(0)
+    copy = import_image(buf, store2, pool2, 11, GEO)
+    assert copy.valid_prefix_blocks() == 21 and copy.saved_tokens == hdr["tokens"]
+    assert store2.pool.owned_blocks(11) == 21
+
+    new_ext = [(5, 4), (50, 17)]
+    plan_in = store2.plan_swap_in(11, new_ext)
+    restored = np.zeros_like(planes)
+    orc.apply_plan("in", restored, pool2, [(o.blocks, o.gpu_start, o.cpu_start)
+                                           for o in plan_in.all_ops()])
+    np.testing.assert_array_equal(restored[:, _table(new_ext)], planes[:, _table(gpu_ext)])
+
+
+def test_corrupt_truncated_and_foreign_images_are_rejected():
+    G, C = 32, 32
+    planes = orc.kv_pattern(4, GEO.num_planes, G, GEO.plane_chunk_bytes)
+    store, pool = CpuStore(C), np.zeros((C, GEO.block_bytes), np.uint8)
+    plan = store.plan_swap_out(1, 6, [(2, 6)])
+    orc.apply_plan("out", planes, pool, [(o.blocks, o.gpu_start, o.cpu_start) for o in plan.ops])
+    buf = io.BytesIO()
+    export_image(store, pool, 1, GEO, buf)
+    raw = bytearray(buf.getvalue())
+
+    flipped = bytearray(raw)
+    flipped[-100] ^= 0x40
+    with pytest.raises(KVImageError, match="corrupt"):
+        import_image(io.BytesIO(bytes(flipped)), CpuStore(C), pool.copy(), 1, GEO)
+    with pytest.raises(KVImageError, match="truncated"):
+        import_image(io.BytesIO(bytes(raw[:-10])), CpuStore(C), pool.copy(), 1, GEO)
+    with pytest.raises(KVImageError, match="magic"):
+        import_image(io.BytesIO(b"NOTIMAGE" + bytes(raw[8:])), CpuStore(C), pool.copy(), 1, GEO)
+    other = KVGeometry("img", num_layers=3, num_kv_heads=2, head_dim=8, tp=2)
+    with pytest.raises(KVImageError, match="geometry"):
+        import_image(io.BytesIO(bytes(raw)), CpuStore(C), np.zeros((C, other.block_bytes),
+                                                                   np.uint8), 1, other)
