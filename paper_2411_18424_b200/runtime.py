@@ -63,7 +63,7 @@ class Runtime:
                  device="cuda:0", copy_impl: str = "kernel", write_kv: bool = True,
                  verify: bool = False, timing: bool = False,
                  duplex_policy: str = "latency", sm_partition: int = 0,
-                 layered_swap_in: bool = False) -> None:
+                 layered_swap_in: bool = False, **executor_kw) -> None:
         if geometry.split_kv:
             raise ValueError("runtime token writes assume fused K/V planes")
         self.geometry = geometry
@@ -72,7 +72,7 @@ class Runtime:
         self.dataplane = SwapDataPlane(self.cache, self.host)
         self.executor = StreamExecutor(self.dataplane, copy_impl=copy_impl, timing=timing,
                                        duplex_policy=duplex_policy, sm_partition=sm_partition,
-                                       layered_swap_in=layered_swap_in)
+                                       layered_swap_in=layered_swap_in, **executor_kw)
         self.write_kv = write_kv
         self.verify = verify
         self.verified = 0

@@ -246,7 +246,7 @@ class StreamExecutor:
     def __init__(self, dataplane, compute_stream=None, copy_impl: str = "kernel",
                  timing: bool = False, duplex_policy: str = "latency",
                  op_granular: bool = True, sm_partition: int = 0,
-                 layered_swap_in: bool = False) -> None:
+                 layered_swap_in: bool = False, flag_ring: int = FLAG_RING) -> None:
         import torch
 
         if copy_impl not in COPY_IMPLS:
@@ -288,7 +288,8 @@ class StreamExecutor:
         self.plan_waits = 0
         self.last_barrier: list[tuple] = []
         self.block_bytes = dataplane.geometry.block_bytes
-        self._flags = torch.zeros(FLAG_RING, dtype=torch.int32, device=dev)
+        self.flag_ring = flag_ring
+        self._flags = torch.zeros(flag_ring, dtype=torch.int32, device=dev)
         self._flags_ptr = self._flags.data_ptr()
         self._flag_head = 0
         self._seq = 0
@@ -316,7 +317,9 @@ class StreamExecutor:
         self.pending = [r for r in self.pending if not r.poll()]
 
     def _claim_flags(self, n: int) -> int:
-        if self._flag_head + n > FLAG_RING:
+        if n > self.flag_ring:
+            raise ValueError(f"a transfer needs {n} completion words, ring holds {self.flag_ring}")
+        if self._flag_head + n > self.flag_ring:
             self._flag_head = 0
         base = self._flag_head
         for r in self.pending:  # never recycle slots a live transfer still signals

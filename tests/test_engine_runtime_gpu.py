@@ -221,3 +221,24 @@ def test_live_attention_reads_catch_corruption(cuda_ok):
     with pytest.raises(KVIntegrityError):
         eng.run()
     rt.close()
+
+
+def test_live_engine_flag_ring_wraps(cuda_ok):
+    """A tiny completion-word ring wraps many times during a live run: slots
+    are only recycled once the transfer that owned them has landed, so every
+    op / plane wait still sees its own transfer (bytes verified)."""
+    from paper_2411_18424_b200.live import DecodeEmulator, LiveEngine, b200_transfer_params
+
+    convs = generate(WorkloadConfig(num_conversations=10, seed=5, max_context_tokens=2048,
+                                    arrival_rate_per_s=20.0, think_time_mean_s=0.05))
+    cfg = EngineConfig(gpu_pool=PoolConfig(total_blocks=128, initial_group_blocks=40),
+                       trace=PriorityTrace(pattern="random", frequency=0.04, seed=2),
+                       ablation="full", cpu_pool_blocks=4096, transfer=b200_transfer_params())
+    rt = _runtime(cfg, layered_swap_in=True, flag_ring=64)
+    dec = DecodeEmulator("cuda:0", weight_bytes=1 << 30)
+    eng = LiveEngine(cfg, convs, rt, dec, layered=True)
+    rep = eng.run()
+    assert rep.total_tokens == rep.expected_tokens and rt.verified > 0
+    assert rt.executor._seq * 3 > 64  # many more completion words than ring slots
+    assert rt.kv_errors() == 0
+    rt.close()
