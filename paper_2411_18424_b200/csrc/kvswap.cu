@@ -106,8 +106,16 @@ __device__ __forceinline__ unsigned long long take_budget(unsigned long long* bu
   return atomicAdd(bucket, static_cast<unsigned long long>(cost));
 }
 
+// Release fence at system scope: this thread's (and, after __syncwarp, its
+// warp's) prior writes - host-mapped ones included - are ordered before what
+// it writes next.  acq_rel is all the credit / publish protocol needs; the
+// sequentially consistent __threadfence_system() is stronger than necessary.
+__device__ __forceinline__ void fence_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
 __device__ __forceinline__ void publish(uint32_t* flag, uint32_t seq) {
-  __threadfence_system();
+  fence_sys();  // acquire the counter's release sequence, release to the flag's readers
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
 }
 
@@ -120,7 +128,7 @@ __device__ __forceinline__ void credit_group(const SwapParams<CAP>& p, uint32_t 
   if (p.plane_flags == nullptr || n == 0) return;
   __syncwarp();  // every lane's stores precede lane 0's fence
   if (lane == 0) {
-    __threadfence_system();
+    fence_sys();
     const uint32_t first = grp * p.layer_group;
     const uint32_t g_here = min(p.layer_group, p.num_planes - first);
     const unsigned long long want =
@@ -143,7 +151,7 @@ __device__ __forceinline__ void credit_op(const SwapParams<CAP>& p, uint32_t lan
   if (p.op_flags == nullptr || n == 0 || op < 0) return;
   __syncwarp();
   if (lane == 0) {
-    __threadfence_system();
+    fence_sys();
     if (atomicAdd(p.op_ctr + op, n) + n == want) {
       p.op_ctr[op] = 0;  // counted in full: reset for the next launch
       publish(p.op_flags + op, p.seq);
