@@ -114,6 +114,13 @@ def main():
                         {"out": 0.0, "in": 0.0}, "kernel", ("out", "in")))
         configs.append(("duplex_paced", "lsu", {"out": (8, 512), "in": (8, 256)},
                         {"out": 52.0, "in": 0.0}, "kernel", ("out", "in")))
+    elif sweep == "policy":
+        configs.append(("in8x256", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 0.0, "in": 0.0}, "kernel", ("in",)))
+        configs.append(("out8x512p52", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 52.0, "in": 0.0}, "kernel", ("out",)))
+        configs.append(("duplex", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 52.0, "in": 0.0}, "kernel", ("out", "in")))
     elif sweep == "in":
         for ct in ((16, 512), (32, 128), (64, 64), (148, 32)):
             for pace in (0.0, 48.0, 40.0):
