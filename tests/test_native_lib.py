@@ -67,6 +67,22 @@ def test_argument_validation_without_gpu():
     h, d = ctypes.c_void_p(), ctypes.c_void_p()
     assert lib.kvs_host_alloc(0, -1, 0, ctypes.byref(h), ctypes.byref(d)) == _lib.KVS_ERR_INVALID
     assert lib.kvs_stream_read(0, 0, None, 0, 0, 0, None) == _lib.KVS_ERR_INVALID
+    # entry points added for layered admission, pacing priority, SM partition, workload
+    sig = _lib.KvsSignals(None, None, None, 1, 0)
+    assert lib.kvs_swap_signaled(None, 0, None, 0, 0, ctypes.byref(sig)) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_swap_signaled(None, 0, None, 0, 0, None) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_swap_ops(None, 0, None, 0, 0, None, None, 0) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_swap_layered(None, 0, None, 0, 0, None, 0) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_set_layer_group(None, 0) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_set_budget_priority(None, 1) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_set_pace(None, 0, 1.0) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_set_budget(None, 1.0) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_set_path(None, 0, 0, 0, 0) == _lib.KVS_ERR_INVALID
+    s, r = (ctypes.c_uint64 * 2)(), ctypes.c_uint64()
+    sms = (ctypes.c_int * 2)()
+    assert lib.kvs_sm_partition(-1, 8, 2, 0, 0, s, ctypes.byref(r), sms) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_sm_partition(0, 8, 0, 0, 0, s, ctypes.byref(r), sms) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_kv_tokens(None, 0, None, 0, 16, 0, -1, 0, None) == _lib.KVS_ERR_INVALID
 
 
 def test_check_maps_codes_to_reference_exceptions():
