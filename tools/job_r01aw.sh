@@ -1,4 +1,6 @@
 #!/bin/bash
+# Probe (removed afterwards): an unbudgeted "latency_partitioned" policy. Result: the 60 GB/s
+# budget is not binding on the 8-SM partition (duplex 50.8 + 27.8 GB/s at +8.7% either way).
 cd "$GRAFT_REPO_ROOT"
 KVS_SERVING_POLICY=latency_partitioned timeout 900 python bench.py --no-sweep --no-trace --no-cpu-baseline > gpurun_out/bench_aw.json 2> gpurun_out/bench_aw.err; tail -2 gpurun_out/bench_aw.err
 python -c "
