@@ -139,18 +139,19 @@ int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
              uint64_t stream, uint32_t* done_flag, uint32_t seq);
 
 /* Layer-wise pipelined swap: same bytes as kvs_swap, moved
- * plane-major (all blocks of plane 0 first, ...), and plane_flags[p] (device
- * or mapped, num_planes words) receives `seq` with system-scope release as
- * soon as plane p has fully landed, so decode of layer l can start (after
- * kvs_wait_flag(stream, plane_flags + l, seq)) while later layers are still
- * in flight.  The reference swaps iteration-wise. */
+ * plane-major in groups of planes (kvs_set_layer_group: all blocks of group 0
+ * first, ...), and plane_flags[p] (device or mapped, num_planes words)
+ * receives `seq` with system-scope release as soon as p's group has fully
+ * landed, so decode of layer l can start (after kvs_wait_flag(stream,
+ * plane_flags + l, seq)) while later layers are still in flight.  The
+ * reference swaps iteration-wise. */
 int kvs_swap_layered(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
                      uint64_t stream, uint32_t* plane_flags, uint32_t seq);
 
 /* Plane-major order granularity of kvs_swap_layered / plane-flagged
  * kvs_swap_signaled: planes are moved in groups of `planes` (block-major
  * inside a group), 0 = auto (>= 256 KiB of a block per group, so host reads
- * stay long).  Plane l's flag still fires once plane l landed. */
+ * stay long).  Plane l's flag fires once every plane of its group landed. */
 int kvs_set_layer_group(KvsHandle* h, int planes);
 
 /* Op-granular completion (SURVEY §7 hard part 4): same bytes as kvs_swap;
@@ -175,7 +176,9 @@ typedef struct KvsSignals {
 
 /* One SwapPlan with any combination of the completion words above: a resumed
  * request can join decode layer by layer (plane flags) while conflicting
- * grants still wait per TransferOp (op flags).  Replaces, together:
+ * grants still wait per TransferOp (op flags).  With plane flags the order is
+ * plane-major, so a TransferOp completes only with its last plane: its op
+ * flag is then published when the whole call has landed.  Replaces, together:
  * engine.py:376-384 (swap-in completion, iteration-wise in the reference,
  * PAPER.md:103-105) and swap.py:236-252 (per-op conflict resolution). */
 int kvs_swap_signaled(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
