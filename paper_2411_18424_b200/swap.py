@@ -15,7 +15,9 @@ Two layers, one object:
    paper's dispatch thread pool, becomes unnecessary: dispatch
    is O(1) per plan).  Real hazards are enforced with CUDA events, independent
    of simulated time:
-     * swap-out waits for the compute stream (the KV it reads was produced there);
+     * both directions wait for the compute work queued before them (swap-out
+       reads the KV compute produced; swap-in must not overtake compute's
+       writes to blocks freed without a swap-out);
      * a transfer waits for any still-running opposite-direction transfer
        whose GPU or host extents it would overwrite or read stale
        (WAR/RAW/WAW; same-direction transfers are already stream-ordered);
@@ -345,8 +347,13 @@ class StreamExecutor:
         gpu = [(op.gpu_start, op.blocks) for op in ops]
         host = [(op.cpu_start, op.blocks) for op in ops]
         stream = self.streams[direction]
-        if direction == "out":
-            stream.wait_stream(self.compute)
+        # Both directions start after the compute work already queued: a
+        # swap-out reads KV that compute produced; a swap-in may overwrite
+        # blocks compute last wrote for a request that just finished or was
+        # dropped for recompute (freed without a swap-out, engine.py:409-414,
+        # 538-545), so it must not overtake those writes (WAW).  Compute that
+        # is queued later (per-layer waits, barriers) is not waited for.
+        stream.wait_stream(self.compute)
         deps = 0
         for r in self.pending:
             if r.direction == direction:

@@ -1,0 +1,80 @@
+"""Randomized hazard test of the StreamExecutor: compute writes, swap-outs and
+swap-ins on overlapping GPU and host extents, issued without host syncs,
+must leave exactly what a sequential (program-order) numpy model leaves.
+Exercises the cross-stream waits (compute -> both directions, WAR/RAW/WAW
+between directions, op- and plane-granular compute barriers)."""
+
+import numpy as np
+import pytest
+
+from oracle import bytes_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _extent_ops(rng, G, C, max_ops=3, max_len=6):
+    """1..max_ops TransferOps at random positions; ops overlapping an earlier
+    op of the same plan (GPU or host side) are dropped."""
+    from paper_2411_18424_b200.cpu_store import TransferOp
+
+    kept = []
+    for _ in range(int(rng.integers(1, max_ops + 1))):
+        L = int(rng.integers(1, max_len + 1))
+        op = TransferOp(L, int(rng.integers(0, G - L + 1)), int(rng.integers(0, C - L + 1)))
+        if all(op.gpu_start + L <= k.gpu_start or k.gpu_start + k.blocks <= op.gpu_start
+               for k in kept) and \
+           all(op.cpu_start + L <= k.cpu_start or k.cpu_start + k.blocks <= op.cpu_start
+               for k in kept):
+            kept.append(op)
+    return kept
+
+
+@pytest.mark.parametrize("mode", ["ops", "layered", "bulk"])
+def test_random_interleavings_match_program_order(cuda_ok, mode):
+    torch = cuda_ok
+    from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
+    from paper_2411_18424_b200.geometry import KVGeometry
+    from paper_2411_18424_b200.swap import StreamExecutor
+
+    geo = KVGeometry("fuzz", num_layers=3, num_kv_heads=1, head_dim=512)  # 32 KiB chunks
+    G = C = 48
+    cache = PagedKVCache(geo, G, device="cuda:0")
+    host = HostKVPool(C, geo.block_bytes)
+    dp = SwapDataPlane(cache, host)
+    ex = StreamExecutor(dp, duplex_policy="throughput" if mode == "bulk" else "latency",
+                        layered_swap_in=mode == "layered")
+    rng = np.random.default_rng({"ops": 1, "layered": 2, "bulk": 3}[mode])
+    gpu = np.zeros((geo.num_planes, G, geo.plane_chunk_bytes), np.uint8)
+    hostm = np.zeros((C, geo.block_bytes), np.uint8)
+    cache.planes.zero_()
+    host.array[:] = 0
+    torch.cuda.synchronize()
+    for step in range(400):
+        a = rng.random()
+        if a < 0.35:  # compute writes one value into a GPU extent
+            L = int(rng.integers(1, 5))
+            s = int(rng.integers(0, G - L + 1))
+            val = int(rng.integers(1, 255))
+            ex.compute_barrier([(s, L)])
+            with torch.cuda.stream(ex.compute):
+                if rng.random() < 0.5:
+                    torch.cuda._sleep(300_000)  # compute lags: later swaps must still wait
+                cache.planes[:, s:s + L].fill_(val)
+            gpu[:, s:s + L] = val
+        elif a < 0.7:
+            ops = _extent_ops(rng, G, C)
+            ex.submit("out", ops)
+            orc.apply_plan("out", gpu, hostm, [(o.blocks, o.gpu_start, o.cpu_start) for o in ops])
+        else:
+            ops = _extent_ops(rng, G, C)
+            ex.submit("in", ops)
+            orc.apply_plan("in", gpu, hostm, [(o.blocks, o.gpu_start, o.cpu_start) for o in ops])
+        if step % 97 == 96:
+            ex.synchronize()
+            np.testing.assert_array_equal(cache.planes.cpu().numpy(), gpu)
+            np.testing.assert_array_equal(host.array, hostm)
+    ex.synchronize()
+    np.testing.assert_array_equal(cache.planes.cpu().numpy(), gpu)
+    np.testing.assert_array_equal(host.array, hostm)
+    assert ex.launches > 100
+    host.close()
