@@ -29,7 +29,7 @@ def _extent_ops(rng, G, C, max_ops=3, max_len=6):
     return kept
 
 
-@pytest.mark.parametrize("mode", ["ops", "layered", "bulk"])
+@pytest.mark.parametrize("mode", ["ops", "layered", "bulk", "partition"])
 def test_random_interleavings_match_program_order(cuda_ok, mode):
     torch = cuda_ok
     from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
@@ -42,8 +42,9 @@ def test_random_interleavings_match_program_order(cuda_ok, mode):
     host = HostKVPool(C, geo.block_bytes)
     dp = SwapDataPlane(cache, host)
     ex = StreamExecutor(dp, duplex_policy="throughput" if mode == "bulk" else "latency",
-                        layered_swap_in=mode == "layered")
-    rng = np.random.default_rng({"ops": 1, "layered": 2, "bulk": 3}[mode])
+                        layered_swap_in=mode == "layered", sm_partition=8 if mode == "partition" else 0)
+    rng = np.random.default_rng({"ops": 1, "layered": 2, "bulk": 3, "partition": 4}[mode])
+    last_in = None
     gpu = np.zeros((geo.num_planes, G, geo.plane_chunk_bytes), np.uint8)
     hostm = np.zeros((C, geo.block_bytes), np.uint8)
     cache.planes.zero_()
@@ -65,10 +66,28 @@ def test_random_interleavings_match_program_order(cuda_ok, mode):
             ops = _extent_ops(rng, G, C)
             ex.submit("out", ops)
             orc.apply_plan("out", gpu, hostm, [(o.blocks, o.gpu_start, o.cpu_start) for o in ops])
-        else:
+        elif a < 0.9 or last_in is None or mode != "layered":
             ops = _extent_ops(rng, G, C)
-            ex.submit("in", ops)
+            last_in = (ex.submit("in", ops), ops)
             orc.apply_plan("in", gpu, hostm, [(o.blocks, o.gpu_start, o.cpu_start) for o in ops])
+        else:
+            # layered join: compute writes plane l of the latest swap-in's blocks as
+            # soon as plane l has landed (kvs_swap_signaled plane flags)
+            rec, ops = last_in
+            # as the engine does: other transfers on these blocks per op, the
+            # joining swap-in itself per plane
+            ex.compute_barrier([(o.gpu_start, o.blocks) for o in ops], skip=(rec,))
+            with torch.cuda.stream(ex.compute):
+                torch.cuda._sleep(100_000)
+            for plane in range(geo.num_planes):
+                ex.wait_plane(ex.compute, rec, plane)
+                val = int(rng.integers(1, 255))
+                with torch.cuda.stream(ex.compute):
+                    for o in ops:
+                        cache.planes[plane, o.gpu_start:o.gpu_start + o.blocks].fill_(val)
+                for o in ops:
+                    gpu[plane, o.gpu_start:o.gpu_start + o.blocks] = val
+            last_in = None
         if step % 97 == 96:
             ex.synchronize()
             np.testing.assert_array_equal(cache.planes.cpu().numpy(), gpu)
