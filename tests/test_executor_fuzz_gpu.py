@@ -4,6 +4,8 @@ must leave exactly what a sequential (program-order) numpy model leaves.
 Exercises the cross-stream waits (compute -> both directions, WAR/RAW/WAW
 between directions, op- and plane-granular compute barriers)."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -29,8 +31,12 @@ def _extent_ops(rng, G, C, max_ops=3, max_len=6):
     return kept
 
 
+SEEDS = int(os.environ.get("KVS_FUZZ_SEEDS", "1"))  # more for a soak run
+
+
+@pytest.mark.parametrize("seed", range(SEEDS))
 @pytest.mark.parametrize("mode", ["ops", "layered", "bulk", "partition"])
-def test_random_interleavings_match_program_order(cuda_ok, mode):
+def test_random_interleavings_match_program_order(cuda_ok, mode, seed):
     torch = cuda_ok
     from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
     from paper_2411_18424_b200.geometry import KVGeometry
@@ -43,7 +49,7 @@ def test_random_interleavings_match_program_order(cuda_ok, mode):
     dp = SwapDataPlane(cache, host)
     ex = StreamExecutor(dp, duplex_policy="throughput" if mode == "bulk" else "latency",
                         layered_swap_in=mode == "layered", sm_partition=8 if mode == "partition" else 0)
-    rng = np.random.default_rng({"ops": 1, "layered": 2, "bulk": 3, "partition": 4}[mode])
+    rng = np.random.default_rng([{"ops": 1, "layered": 2, "bulk": 3, "partition": 4}[mode], seed])
     last_in = None
     gpu = np.zeros((geo.num_planes, G, geo.plane_chunk_bytes), np.uint8)
     hostm = np.zeros((C, geo.block_bytes), np.uint8)
