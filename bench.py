@@ -144,15 +144,14 @@ class ClockSampler:
 # --------------------------------------------------------------------- plans
 
 def make_plans(group: int, seed: int):
-    from oracle.bytes_oracle import random_runs  # seeded plan generator (test infra)
+    from paper_2411_18424_b200.synthetic import pair_tables, random_runs
     rng = np.random.default_rng(seed)
     out_ops = random_runs(rng, PLAN_BLOCKS, group, POOL_BLOCKS, HOST_POOL_BLOCKS)
     in_ops = random_runs(rng, PLAN_BLOCKS, group, POOL_BLOCKS, HOST_POOL_BLOCKS)
     # swap-in reads back exactly the host blocks swap-out wrote
     host_blocks = np.concatenate([np.arange(c, c + b) for b, g, c in out_ops])
     gpu_blocks = np.concatenate([np.arange(g, g + b) for b, g, c in in_ops])
-    from oracle.bytes_oracle import table_to_ops
-    in_ops = table_to_ops(gpu_blocks, host_blocks)
+    in_ops = pair_tables(gpu_blocks, host_blocks)
     return out_ops.astype(np.int32), in_ops.astype(np.int32)
 
 
@@ -417,7 +416,7 @@ def run_e2e(args, geo, dp, dev, barrier, world):
     """Same bytes through CpuStore + SwapManager.dispatch (the drop-in API)."""
     import torch
 
-    from oracle.bytes_oracle import random_runs
+    from paper_2411_18424_b200.synthetic import random_runs
     from paper_2411_18424_b200.costmodel import TransferParams
     from paper_2411_18424_b200.cpu_store import CpuStore
     from paper_2411_18424_b200.swap import StreamExecutor, SwapManager
@@ -550,7 +549,7 @@ def serving_interference(dp, dev, s, sm_partition: int = 0):
 
     import torch
 
-    from oracle.bytes_oracle import random_runs
+    from paper_2411_18424_b200.synthetic import random_runs
     from paper_2411_18424_b200.live import DecodeEmulator
     from paper_2411_18424_b200.swap import DUPLEX_POLICIES
 
@@ -653,7 +652,7 @@ def ce_peak(dev, host, cache):
 
 def group_sweep(dp, s):
     import torch
-    from oracle.bytes_oracle import random_runs
+    from paper_2411_18424_b200.synthetic import random_runs
     geo = dp.geometry
     out = []
     rng = np.random.default_rng(11)

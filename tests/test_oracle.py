@@ -92,3 +92,20 @@ def test_random_runs_are_disjoint():
     g = np.concatenate([np.arange(gs, gs + b) for b, gs, _ in ops])
     c = np.concatenate([np.arange(cs, cs + b) for b, _, cs in ops])
     assert len(set(g)) == 100 and len(set(c)) == 100
+
+
+def test_synthetic_generators_agree_with_the_oracle_restatement():
+    """bench.py / tools build plans with paper_2411_18424_b200.synthetic; the
+    pairing rule must be the oracle's (_pair_extents, cpu_store.py:95-120)."""
+    from paper_2411_18424_b200 import synthetic as syn
+
+    for seed in range(20):
+        rng = np.random.default_rng(seed)
+        g = syn.random_block_table(rng, 300, 1000)
+        c = syn.random_block_table(rng, 300, 1000)
+        runs = np.concatenate([np.arange(s, s + 40) for s in (5, 500, 300)])
+        g2, c2 = np.concatenate([g, runs]), np.concatenate([c, runs + 3])
+        np.testing.assert_array_equal(syn.pair_tables(g2, c2), orc.table_to_ops(g2, c2))
+        a = syn.random_runs(np.random.default_rng(seed), 512, 16, 2048, 2048)
+        b = orc.random_runs(np.random.default_rng(seed), 512, 16, 2048, 2048)
+        np.testing.assert_array_equal(a, b)  # same seeded layout as the oracle's generator

@@ -14,7 +14,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from oracle import bytes_oracle as orc  # noqa: E402  (plan generator only)
+from paper_2411_18424_b200 import synthetic as orc  # noqa: E402  (plan generator)
 from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane  # noqa: E402
 from paper_2411_18424_b200.geometry import PRESETS  # noqa: E402
 
