@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace-convs", type=int, default=64)
     ap.add_argument("--no-trace", action="store_true")
+    ap.add_argument("--trace-pattern", default="vtc", choices=["vtc", "markov", "random"],
+                    help="trace priority pattern (config 3 names VTC; markov is the "
+                         "reference's parity-pinned pattern)")
     ap.add_argument("--no-layered", action="store_true",
                     help="trace: resumed requests join only once all their KV landed")
     ap.add_argument("--sm-partition", type=int, default=8,
@@ -503,10 +506,11 @@ def run_trace(args, geo, dev):
            "cpu_pool": {"total_blocks": 4096},
            "workload": {"num_conversations": args.trace_convs, "arrival_rate_per_s": 4.0,
                         "think_time_mean_s": 2.0},
-           "trace": {"pattern": "markov", "frequency": 0.04}}
+           "trace": {"pattern": args.trace_pattern, "frequency": 0.04}}
     out = {"workload": f"{args.trace_convs} conversations, 4 req/s, think 2 s, 512 x "
                        f"{geo.block_bytes / 2**20:g} MiB GPU blocks per rank (TP{world}), "
-                       f"Markov f=0.04, decode = {decode.bytes_per_us / 1e3:.0f} GB/s weight "
+                       f"{args.trace_pattern} priorities f=0.04 (BASELINE config 3: VTC), "
+                       f"decode = {decode.bytes_per_us / 1e3:.0f} GB/s weight "
                        f"streaming per rank",
            "tp": world, "sm_partition": sms, "runs": {}}
     for name, mode, impl in (("fastswitch", "full", "kernel"),
