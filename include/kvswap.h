@@ -127,6 +127,16 @@ int kvs_set_budget(KvsHandle* h, double gbps);
  * (engine.py:609, conflicts resolved per op). */
 int kvs_set_budget_priority(KvsHandle* h, int dir);
 
+/* STREAM RULE — kvs_swap, kvs_swap_ops, kvs_swap_layered, kvs_swap_signaled:
+ * completion words are published through per-handle, per-direction device
+ * counters (a CTA ticket, op counters, plane-group counters) that each launch
+ * of that direction leaves reset for the next one.  Issue every call of one
+ * direction on one handle on ONE stream (one stream per direction per
+ * handle).  Two streams of the same direction could interleave their tickets
+ * and publish a done / op / plane flag before all of a call's CTAs landed.
+ * The two directions may use two different streams.  Need more concurrency
+ * in one direction: create another handle over the same pools. */
+
 /* Queue one SwapPlan's bytes on `stream` — asynchronous, no host blocking,
  * no allocation.  Replaces the modeled copy-engine timeline of
  * SwapManager.dispatch (swap.py:193-205, costmodel.py:29-31).
@@ -134,7 +144,8 @@ int kvs_set_budget_priority(KvsHandle* h, int dir);
  * done_flag (optional, may be NULL): device-visible uint32 (device memory or
  * mapped host) that receives `seq` with system-scope release once every byte
  * of this call has landed; pair with kvs_wait_flag for cross-stream waits
- * (reference: OpRecord.exec_done / not_before, swap.py:36-42, 186). */
+ * (reference: OpRecord.exec_done / not_before, swap.py:36-42, 186).
+ * Stream rule above applies. */
 int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
              uint64_t stream, uint32_t* done_flag, uint32_t seq);
 
@@ -144,7 +155,7 @@ int kvs_swap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
  * receives `seq` with system-scope release as soon as p's group has fully
  * landed, so decode of layer l can start (after kvs_wait_flag(stream,
  * plane_flags + l, seq)) while later layers are still in flight.  The
- * reference swaps iteration-wise. */
+ * reference swaps iteration-wise.  Stream rule above. */
 int kvs_swap_layered(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
                      uint64_t stream, uint32_t* plane_flags, uint32_t seq);
 
@@ -180,7 +191,8 @@ typedef struct KvsSignals {
  * plane-major, so a TransferOp completes only with its last plane: its op
  * flag is then published when the whole call has landed.  Replaces, together:
  * engine.py:376-384 (swap-in completion, iteration-wise in the reference,
- * PAPER.md:103-105) and swap.py:236-252 (per-op conflict resolution). */
+ * PAPER.md:103-105) and swap.py:236-252 (per-op conflict resolution).
+ * Stream rule above applies. */
 int kvs_swap_signaled(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops,
                       uint64_t stream, const KvsSignals* sig);
 

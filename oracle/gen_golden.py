@@ -59,18 +59,72 @@ ENGINE_CASES = {
                      "transfer": {"bandwidth_bytes_per_us": 63000},
                      "workload": {"arrival_rate_per_s": 2.0, "num_conversations": 60},
                      "trace": {"pattern": "markov", "frequency": 0.04}},
+    # BASELINE config 3: VTC priorities (reference engine + oracle/vtc_oracle.py)
+    "vtc_config3_bench": {"ablation": "full", "block": {"bytes_per_block": 2097152},
+                          "gpu_pool": {"total_blocks": 512},
+                          "workload": {"num_conversations": 64, "arrival_rate_per_s": 4.0,
+                                       "think_time_mean_s": 2.0},
+                          "trace": {"pattern": "vtc", "frequency": 0.04}},
+    "vtc_config3_default": {"ablation": "full", "block": {"bytes_per_block": 2097152},
+                            "gpu_pool": {"total_blocks": 512},
+                            "cpu_pool": {"total_blocks": 8192},
+                            "workload": {"num_conversations": 200, "arrival_rate_per_s": 2.0},
+                            "trace": {"pattern": "vtc", "frequency": 0.04}},
+    "vtc_config3_baseline": {"ablation": "baseline", "block": {"bytes_per_block": 2097152},
+                             "gpu_pool": {"total_blocks": 512},
+                             "workload": {"num_conversations": 64, "arrival_rate_per_s": 4.0,
+                                          "think_time_mean_s": 2.0},
+                             "trace": {"pattern": "vtc", "frequency": 0.04}},
+    "vtc_pressure_lowprio": {"ablation": "full",
+                             "gpu_pool": {"total_blocks": 256,
+                                          "victim_policy": "lowest_priority"},
+                             "cpu_pool": {"total_blocks": 1500},
+                             "workload": {"arrival_rate_per_s": 3.0, "num_conversations": 60},
+                             "trace": {"pattern": "vtc", "frequency": 0.2,
+                                       "vtc_wp": 1, "vtc_wq": 4}},
 }
+# BASELINE config 4: Qwen-2.5-32B KV, per-rank shard bytes at TP 2/4/8
+# (64 layers x 8 KV heads x d 128 x 16 tok x 2 (K,V) x fp16 / TP), multi-turn
+# reuse, random priorities f=0.04.
+for _tp in (2, 4, 8):
+    ENGINE_CASES[f"c4_qwen32b_tp{_tp}"] = {
+        "ablation": "full", "block": {"bytes_per_block": 4194304 // _tp},
+        "gpu_pool": {"total_blocks": 1024}, "cpu_pool": {"total_blocks": 8192},
+        "workload": {"num_conversations": 60, "arrival_rate_per_s": 2.0},
+        "trace": {"pattern": "random", "frequency": 0.04}}
+# BASELINE config 5: LLaMA-3-70B TP8 rank shard (655360 B per block), 32K
+# context, high preemption.  The reference's deadlock detector fires on
+# legitimately long swaps here (engine.py:48, :536-538): both engines run it
+# with DEADLOCK_ITERATIONS = 1000.
+ENGINE_CASES["c5_llama70b_tp8"] = {
+    "ablation": "full", "block": {"bytes_per_block": 655360},
+    "gpu_pool": {"total_blocks": 8192, "initial_group_blocks": 60},
+    "cpu_pool": {"total_blocks": 65536},
+    "workload": {"num_conversations": 64, "arrival_rate_per_s": 1.0,
+                 "input_tokens": {"median": 6000.0, "sigma": 0.9, "max": 16384},
+                 "max_context_tokens": 32768},
+    "trace": {"pattern": "random", "frequency": 0.04}}
+DEADLOCK_ITERATIONS = {"c5_llama70b_tp8": 1000}
 
 
 def engine_goldens(kv):
     from kvswitch import config as C
+    from kvswitch import engine as ref_engine
     from kvswitch.alloc import PoolConfig
     from kvswitch.engine import Engine, EngineConfig
     from kvswitch.scheduler import PriorityTrace
     from kvswitch.workload import Conversation
 
+    from oracle import vtc_oracle
+
     out = {}
     for name, doc in ENGINE_CASES.items():
+        make = Engine
+        if doc is not None and doc.get("trace", {}).get("pattern") == "vtc":
+            ref_doc, wp, wq = vtc_oracle.reference_doc(doc)
+            make = vtc_oracle.vtc_reference_engine(ref_engine, wp, wq)
+        else:
+            ref_doc = doc
         if doc is None:
             cfg = EngineConfig(gpu_pool=PoolConfig(total_blocks=48, initial_group_blocks=20),
                                trace=PriorityTrace(pattern="random", frequency=0.2, seed=1),
@@ -78,9 +132,9 @@ def engine_goldens(kv):
             convs = [Conversation(0, [(320, 320)], 0, 0), Conversation(1, [(320, 320)], 1000, 0)]
             settings_doc = {"special": "duel"}
         else:
-            s = C.build(doc)
+            s = C.build(ref_doc)
             cfg, convs, settings_doc = s.engine, kv.generate(s.workload), s.doc
-        eng = Engine(cfg, convs)
+        eng = make(cfg, convs)
         plans = []
         orig = eng.manager.dispatch
 
@@ -91,10 +145,16 @@ def engine_goldens(kv):
             return _orig(clock, iteration, plan, not_before)
 
         eng.manager.dispatch = spy
-        report = eng.run()
+        saved = ref_engine.DEADLOCK_ITERATIONS
+        ref_engine.DEADLOCK_ITERATIONS = DEADLOCK_ITERATIONS.get(name, saved)
+        try:
+            report = eng.run()
+        finally:
+            ref_engine.DEADLOCK_ITERATIONS = saved
         events = [[e.iteration, e.request, e.direction, e.ops, e.blocks, e.dispatch_done,
                    e.exec_done] for e in eng.manager.events_log]
-        out[name] = {"doc": doc, "report": json.loads(report.to_json()),
+        out[name] = {"doc": doc, "deadlock_iterations": DEADLOCK_ITERATIONS.get(name),
+                     "report": json.loads(report.to_json()),
                      "events_sha256": h(events), "plans_sha256": h(plans),
                      "n_events": len(events), "first_plans": plans[:20],
                      "gpu_dump_sha256": h(eng.pool.dump()),
@@ -283,6 +343,7 @@ def workload_goldens(kv):
 
 def main():
     sys.path.insert(0, str(REF))
+    sys.path.insert(0, str(OUT.parents[1]))
     import kvswitch as kv
     from kvswitch import alloc, cpu_store
 

@@ -41,7 +41,8 @@ def default_config() -> dict:
                      "output_tokens": {"median": 112.0, "sigma": 0.7, "max": 512},
                      "think_time_mean_s": 10.0, "max_context_tokens": 3072,
                      "trace_path": None},
-        "trace": {"pattern": "markov", "frequency": 0.02, "p_keep": 0.8},
+        "trace": {"pattern": "markov", "frequency": 0.02, "p_keep": 0.8,
+                  "vtc_wp": 1, "vtc_wq": 2},
         "swap_policy": {"sync_threshold_ratio": 0.5, "short_request_blocks": 16},
         "reuse": {"prealloc_min_blocks": 8, "prealloc_max_blocks": 256,
                   "release_copy_on_swap_in": False},

@@ -598,8 +598,10 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   p.ticket = h->d_tickets + dir;
   p.ticket_base = h->ticket_next[dir];
   p.seq = o.seq;
-  if (o.done_flag != nullptr || (!bulk && o.layered && o.op_flags != nullptr))
-    h->ticket_next[dir] += static_cast<unsigned long long>(ctas);
+  // The host ticket advances only once the launch is accepted: a failed
+  // attribute call or launch must not leave it ahead of the device ticket
+  // (every later done / end-of-plan flag of this direction would never fire).
+  const bool ticketed = o.done_flag != nullptr || (!bulk && o.layered && o.op_flags != nullptr);
   if (bulk) {
     const size_t smem = static_cast<size_t>(stages) * static_cast<size_t>(piece);
     auto kern = dir == KVS_DIR_OUT ? kvs_swap_bulk_kernel<KVS_DIR_OUT, CAP>
@@ -613,8 +615,11 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   } else {
     kvs_swap_kernel<KVS_DIR_IN, CAP><<<ctas, threads, 0, stream>>>(p);
   }
+  const int rc = cuda_rc(cudaGetLastError());
+  if (rc) return rc;
+  if (ticketed) h->ticket_next[dir] += static_cast<unsigned long long>(ctas);
   h->launches += 1;
-  return cuda_rc(cudaGetLastError());
+  return KVS_OK;
 }
 
 // One launch for <= 2048 ops, smallest parameter block that fits.

@@ -14,6 +14,12 @@ swapped KV across a restart.  The reference keeps copies in memory only
 
 Layout: 8-byte magic, little-endian u32 header length, UTF-8 JSON header,
 then `blocks * block_bytes` raw bytes.
+
+Both directions touch pool rows from the CPU.  Pass the `StreamExecutor`
+that moves this pool's bytes: the rows are fenced against its in-flight
+transfers first (a swap-out still writing the exported rows, or a swap-in
+still reading rows the import is about to overwrite).  Without an executor
+the caller guarantees no transfer touches the pool.
 """
 
 from __future__ import annotations
@@ -26,7 +32,7 @@ from typing import BinaryIO, Optional, Union
 
 import numpy as np
 
-from .cpu_store import CpuCopy, CpuStore, Segment
+from .cpu_store import CpuCopy, CpuOutOfMemoryError, CpuStore, Segment
 from .geometry import KVGeometry
 
 MAGIC = b"KVSIMG01"
@@ -41,12 +47,22 @@ def _geometry_doc(g: KVGeometry) -> dict:
     return asdict(g)
 
 
+def _runs(rows: list[int]) -> list[tuple[int, int]]:
+    out: list[tuple[int, int]] = []
+    for r in rows:
+        if out and out[-1][0] + out[-1][1] == r:
+            out[-1] = (out[-1][0], out[-1][1] + 1)
+        else:
+            out.append((r, 1))
+    return out
+
+
 def export_image(store: CpuStore, pool: np.ndarray, req: int, geometry: KVGeometry,
-                 out: Union[str, BinaryIO]) -> dict:
+                 out: Union[str, BinaryIO], executor=None) -> dict:
     """Write request `req`'s valid host-image prefix; returns the header.
 
     pool: uint8 [num_cpu_blocks, block_bytes] view of the host pool
-    (`HostKVPool.array`)."""
+    (`HostKVPool.array`); executor: see the module docstring."""
     if pool.ndim != 2 or pool.shape[1] != geometry.block_bytes:
         raise ValueError("pool rows must be geometry.block_bytes wide")
     copy = store.copy_of(req)
@@ -60,13 +76,17 @@ def export_image(store: CpuStore, pool: np.ndarray, req: int, geometry: KVGeomet
         rows.extend(range(phys, phys + min(hi, blocks) - lo))
     if len(rows) != blocks:
         raise KVImageError(f"request {req}: valid prefix of {blocks} blocks is not backed")
+    if executor is not None and rows:
+        executor.host_fence(_runs(rows))
     data = pool[np.asarray(rows, dtype=np.int64)] if rows else pool[:0]
     header = {
         "magic": MAGIC.decode(), "version": VERSION, "request": int(req),
         "geometry": _geometry_doc(geometry), "block_bytes": geometry.block_bytes,
         "blocks": blocks,
-        "tokens": copy.saved_tokens if copy.saved_tokens is not None
-        else blocks * geometry.block_tokens,
+        # a contaminated copy exports only its valid prefix: never claim
+        # tokens past it (plan_swap_in_prefix clamps the same way)
+        "tokens": min(copy.saved_tokens, blocks * geometry.block_tokens)
+        if copy.saved_tokens is not None else blocks * geometry.block_tokens,
         "crc32": [zlib.crc32(row) for row in data],
     }
     blob = json.dumps(header, sort_keys=True).encode()
@@ -109,8 +129,15 @@ def read_image(src: Union[str, BinaryIO]) -> tuple[dict, np.ndarray]:
 
 
 def import_image(src: Union[str, BinaryIO], store: CpuStore, pool: np.ndarray, req: int,
-                 geometry: KVGeometry) -> CpuCopy:
-    """Place an image in `store`'s host pool as request `req`'s CPU copy."""
+                 geometry: KVGeometry, rank: Optional[int] = None,
+                 executor=None) -> CpuCopy:
+    """Place an image in `store`'s host pool as request `req`'s CPU copy.
+
+    Room is made by evicting lower-priority copies (cpu_store.py evict_for)
+    only when the request's priority is known: `rank`, or an existing
+    `store.ranks` entry.  Otherwise the import takes free blocks only and
+    raises CpuOutOfMemoryError when they do not suffice — an unranked import
+    must not contaminate every other request's copy."""
     header, data = read_image(src)
     if header["geometry"] != _geometry_doc(geometry):
         raise KVImageError(f"image geometry {header['geometry']} != this rank's "
@@ -120,9 +147,17 @@ def import_image(src: Union[str, BinaryIO], store: CpuStore, pool: np.ndarray, r
     blocks = int(header["blocks"])
     copy = CpuCopy(owner=req, saved_tokens=int(header["tokens"]))
     if blocks:
-        store._ensure_free(req, blocks)
+        if rank is not None:
+            store.set_rank(req, rank)
+        if req in store.ranks:
+            store._ensure_free(req, blocks)
+        elif store.pool.free_blocks < blocks:
+            raise CpuOutOfMemoryError(f"cannot host {blocks} blocks for unranked request {req}")
+        groups = store.pool.allocate(req, blocks, reclaim=False).groups
+        if executor is not None:
+            executor.host_fence([(g.start, g.length) for g in groups])
         pos = 0
-        for g in store.pool.allocate(req, blocks, reclaim=False).groups:
+        for g in groups:
             pool[g.start:g.start + g.length] = data[pos:pos + g.length]
             copy.segments.append(Segment(pos, pos + g.length, g.id, True))
             pos += g.length

@@ -441,6 +441,20 @@ class StreamExecutor:
     def wait_transfer(self, rec: TransferRecord) -> None:
         self.compute.wait_event(rec.event)
 
+    def host_fence(self, rows: list[tuple[int, int]]) -> int:
+        """Block the calling host thread until every pending transfer whose
+        host extents overlap `rows` ([(start, length)] host blocks) is done,
+        so the CPU may read or write those pool rows.  Returns how many
+        transfers it waited for."""
+        self._prune()
+        n = 0
+        for r in self.pending:
+            if _overlaps(rows, r.host):
+                r.event.synchronize()
+                n += 1
+        self._prune()
+        return n
+
     def synchronize(self) -> None:
         for s in self.streams.values():
             s.synchronize()

@@ -77,8 +77,11 @@ def _engine_for(name, doc):
 
 
 @pytest.mark.parametrize("name", sorted(load("engine.json")))
-def test_engine_matches_reference(name):
+def test_engine_matches_reference(name, monkeypatch):
     want = load("engine.json")[name]
+    if want.get("deadlock_iterations"):  # config 5: engine.py:48 patched in both engines
+        from paper_2411_18424_b200 import engine as engine_mod
+        monkeypatch.setattr(engine_mod, "DEADLOCK_ITERATIONS", want["deadlock_iterations"])
     eng = _engine_for(name, want["doc"])
     plans = []
     orig = eng.manager.dispatch

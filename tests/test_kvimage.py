@@ -70,3 +70,70 @@ def test_corrupt_truncated_and_foreign_images_are_rejected():
     with pytest.raises(KVImageError, match="geometry"):
         import_image(io.BytesIO(bytes(raw)), CpuStore(C), np.zeros((C, other.block_bytes),
                                                                    np.uint8), 1, other)
+
+
+def test_contaminated_copy_exports_only_the_tokens_its_prefix_holds():
+    """the header's token count is clamped to the exported blocks,
+    so a resumer never skips recompute it owes (plan_swap_in_prefix rule)."""
+    C = 40
+    store, pool = CpuStore(C), np.zeros((C, GEO.block_bytes), np.uint8)
+    store.set_rank(1, 5)
+    store.plan_swap_out(1, 10, [(0, 10)], tokens=160)
+    store.plan_swap_out(1, 30, [(0, 30)], tokens=30 * 16 - 3)
+    store.evict_for(0, 15)  # a better-ranked request takes the 20-block tail segment
+    assert store.copy_of(1).valid_prefix_blocks() == 10
+    buf = io.BytesIO()
+    hdr = export_image(store, pool, 1, GEO, buf)
+    assert hdr["blocks"] == 10 and hdr["tokens"] == 10 * 16
+    buf.seek(0)
+    copy = import_image(buf, CpuStore(C), pool.copy(), 3, GEO)
+    assert copy.saved_tokens == 160 and copy.valid_prefix_blocks() == 10
+
+
+def test_unranked_import_never_evicts_and_ranked_import_does():
+    from paper_2411_18424_b200.cpu_store import CpuOutOfMemoryError
+
+    C = 32
+    store, pool = CpuStore(C), np.zeros((C, GEO.block_bytes), np.uint8)
+    store.plan_swap_out(1, 12, [(0, 12)])
+    buf = io.BytesIO()
+    export_image(store, pool, 1, GEO, buf)
+    raw = buf.getvalue()
+
+    full = CpuStore(C)
+    full.set_rank(9, 3)
+    full.plan_swap_out(9, 25, [(0, 25)])  # 7 free blocks left
+    with pytest.raises(CpuOutOfMemoryError):
+        import_image(io.BytesIO(raw), full, pool.copy(), 4, GEO)
+    assert full.copy_of(9).fully_valid  # nobody was contaminated
+    copy = import_image(io.BytesIO(raw), full, pool.copy(), 4, GEO, rank=0)
+    assert copy.valid_prefix_blocks() == 12
+    assert not full.copy_of(9).fully_valid  # the lower-priority copy paid
+
+
+class _FenceSpy:
+    def __init__(self):
+        self.calls = []
+
+    def host_fence(self, rows):
+        self.calls.append(list(rows))
+        return 0
+
+
+def test_export_and_import_fence_their_pool_rows_on_the_executor():
+    """CPU reads/writes of pool rows wait for in-flight transfers
+    over those rows (StreamExecutor.host_fence)."""
+    C = 64
+    store, pool = CpuStore(C), np.zeros((C, GEO.block_bytes), np.uint8)
+    plan = store.plan_swap_out(2, 9, [(4, 9)])
+    spy = _FenceSpy()
+    buf = io.BytesIO()
+    export_image(store, pool, 2, GEO, buf, executor=spy)
+    cpu = [(o.cpu_start, o.blocks) for o in plan.ops]
+    assert spy.calls == [cpu]
+    buf.seek(0)
+    store2 = CpuStore(C)
+    store2.plan_swap_out(5, 3, [(0, 3)])
+    copy = import_image(buf, store2, np.zeros_like(pool), 6, GEO, executor=spy)
+    placed = [(store2.pool.group(s.group_id).start, s.length) for s in copy.segments]
+    assert spy.calls[1] == placed

@@ -87,13 +87,17 @@ def c3(decode):
 
 
 def c4():
+    """Replay with real bytes.  The decisions are first pinned: the report of
+    the byte-moving run must equal the golden recorded from the reference
+    (tests/golden/engine.json c4_qwen32b_tp*)."""
+    golden = json.loads((Path(__file__).resolve().parents[1] / "tests" / "golden"
+                         / "engine.json").read_text())
     out = {}
     for tp in (2, 4, 8):
         geo = QWEN25_32B.with_tp(tp)
-        doc = {"ablation": "full", "block": {"bytes_per_block": geo.block_bytes},
-               "gpu_pool": {"total_blocks": 1024}, "cpu_pool": {"total_blocks": 8192},
-               "workload": {"num_conversations": 60, "arrival_rate_per_s": 2.0},
-               "trace": {"pattern": "random", "frequency": 0.04}}
+        want = golden[f"c4_qwen32b_tp{tp}"]
+        doc = want["doc"]
+        assert doc["block"]["bytes_per_block"] == geo.block_bytes
         cfg, wl, _ = mconfig.build(doc)
         rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, verify=True,
                      timing=True)
@@ -101,7 +105,10 @@ def c4():
         t0 = time.perf_counter()
         rep = eng.run()
         rt.synchronize()
+        if json.loads(rep.to_json()) != want["report"]:
+            raise AssertionError(f"c4 tp{tp}: replay report differs from the reference golden")
         out[f"tp{tp}"] = {
+            "decisions_match_reference_golden": True,
             "block_bytes_per_rank": geo.block_bytes, "heads_per_rank": geo.heads_per_rank,
             "wall_s": round(time.perf_counter() - t0, 1),
             "moved_out_blocks": rep.swap_out_blocks, "reused_blocks": rep.reused_blocks,
