@@ -1,4 +1,5 @@
-"""KV-swap benchmark (BASELINE.json metric: KV swap GB/s vs PCIe peak per GPU).
+"""KV-swap benchmark (BASELINE.json metric: KV swap GB/s vs PCIe peak per GPU;
+P99 TTFT/TBT on the multi-turn preemption trace).
 
 Workload (N=1, BASELINE config 2 "block-group vs fragmented allocation
 sweep", LLaMA-3-8B KV shape, 1 B200): one step = the swap-out of a
@@ -12,13 +13,17 @@ Inputs (8 GiB per direction) exceed the 126 MB L2: no flush needed.
            KV already resident in HBM / host pool when timing starts.
   e2e    = the same bytes through the public API: CpuStore.plan_swap_out /
            plan_swap_in (control plane) -> SwapManager.dispatch -> kvs_swap,
-           64 requests of 64 blocks, wall clock incl. planning + sync.
-  --impl reference: the oracle's C restatement of the same plans on the
-           host cores (the reference kvswitch is a simulator that moves no
-           bytes), rank 0 only.
+           64 requests of 64 blocks, wall clock incl. planning + sync; the
+           round trip's bytes are verified after the timed steps.
+  --impl reference: the CPU path on the host cores, same plans, same sizes:
+           the oracle's C restatement moves the bytes (the reference kvswitch
+           is a simulator that moves none), and the reference's
+           own control plane (baseline/_ref) is timed per call; rank 0 only.
 
-Multi-GPU: one process per GPU (torchrun); each rank swaps its own KV shard
-over its own PCIe link — no collective on the data path ("scaling": "weak").
+Multi-GPU: one process per GPU; each rank swaps its own KV shard over its own
+PCIe link — no collective on the data path ("scaling": "weak").
+`python bench.py --gpus N` without torchrun relaunches itself under
+torch.distributed.run with N ranks.
 """
 
 from __future__ import annotations
@@ -26,6 +31,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -43,9 +49,28 @@ PCIE_GEN5_X16_GBS = 63.0  # 64 GT/s raw per direction after 128b/130b (BASELINE.
 PLAN_BLOCKS = 4096
 POOL_BLOCKS = 8192
 HOST_POOL_BLOCKS = 5120  # 10 GiB pinned per rank (x8 ranks on one host)
+SWEEP_GROUPS = (1, 2, 4, 8, 16, 32, 64, 128, 256)
 
 
-def parse():
+def pools(plan_blocks: int) -> tuple[int, int]:
+    """(GPU pool, host pool) blocks for a plan size: 8192 / 5120 at config 2's
+    4096-block plans (smaller plans, used only by tests, scale them down)."""
+    return (POOL_BLOCKS * plan_blocks // PLAN_BLOCKS,
+            HOST_POOL_BLOCKS * plan_blocks // PLAN_BLOCKS)
+
+# Live traces (BASELINE config 3): LLaMA-3-8B KV, 512 x 2 MiB GPU blocks.
+# "stress" is the saturated 64-conversation variant; "default" is the
+# reference's default workload size (workload.py:44-53: 200 conversations,
+# think 10 s) at 2 req/s.  Both replay-pinned (tests/golden/engine.json
+# vtc_config3_bench / vtc_config3_default / llama8b-style markov cases).
+TRACES = {
+    "stress_vtc": {"convs": 64, "rate": 4.0, "think": 2.0, "cpu": 4096, "pattern": "vtc"},
+    "stress_markov": {"convs": 64, "rate": 4.0, "think": 2.0, "cpu": 4096, "pattern": "markov"},
+    "default_vtc": {"convs": 200, "rate": 2.0, "think": 10.0, "cpu": 8192, "pattern": "vtc"},
+}
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -54,19 +79,23 @@ def parse():
     ap.add_argument("--model", default="llama3-8b")
     ap.add_argument("--group", type=int, default=16)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--plan-blocks", type=int, default=PLAN_BLOCKS,
+                    help="blocks per plan (default = config 2's 4096; smaller only for tests)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--trace-convs", type=int, default=64)
     ap.add_argument("--no-trace", action="store_true")
-    ap.add_argument("--trace-pattern", default="vtc", choices=["vtc", "markov", "random"],
-                    help="trace priority pattern (config 3 names VTC; markov is the "
-                         "reference's parity-pinned pattern)")
+    ap.add_argument("--traces", default=",".join(TRACES),
+                    help=f"comma list of live traces to run, from {sorted(TRACES)}")
+    ap.add_argument("--trace-convs", type=int, default=0,
+                    help="override every trace's conversation count (tests)")
     ap.add_argument("--no-layered", action="store_true",
                     help="trace: resumed requests join only once all their KV landed")
     ap.add_argument("--sm-partition", type=int, default=8,
                     help="serving + trace: swap kernels on their own N-SM green context, "
                          "decode on the rest (0 = share all SMs)")
-    return ap.parse_args()
+    ap.add_argument("--e2e-policy", default="throughput",
+                    help="StreamExecutor duplex policy of the headline e2e leg")
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -74,6 +103,31 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch_if_needed(args) -> None:
+    """`--gpus N` without a launcher: become N ranks under torch.distributed.run
+    (127.0.0.1 rendezvous).  Under a launcher, WORLD_SIZE must equal --gpus."""
+    if "WORLD_SIZE" not in os.environ:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                   "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+                   *sys.argv[1:]]
+            raise SystemExit(subprocess.call(cmd))
+        return
+    _, world, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started "
+                         f"WORLD_SIZE={world} ranks")
 
 
 def cpu_model() -> str:
@@ -84,6 +138,26 @@ def cpu_model() -> str:
     except OSError:
         pass
     return "unknown"
+
+
+def host_cpu_info(threads: int) -> dict:
+    """Where the CPU baseline ran: cores, model, NUMA nodes and the node of
+    the calling thread (its buffers are first-touched there)."""
+    node = None
+    try:
+        cpu = os.sched_getcpu()
+        for d in Path(f"/sys/devices/system/cpu/cpu{cpu}").glob("node*"):
+            node = int(d.name[4:])
+    except (OSError, AttributeError, ValueError):
+        pass
+    try:
+        nodes = len(list(Path("/sys/devices/system/node").glob("node[0-9]*"))) or 1
+    except OSError:
+        nodes = 1
+    if node is None and nodes == 1:
+        node = 0
+    return {"cores": threads, "cpu_count": os.cpu_count(), "cpu_model": cpu_model(),
+            "numa_node": node, "numa_nodes": nodes}
 
 
 # --------------------------------------------------------------------- clocks
@@ -146,45 +220,125 @@ class ClockSampler:
 
 # --------------------------------------------------------------------- plans
 
-def make_plans(group: int, seed: int):
-    from paper_2411_18424_b200.synthetic import pair_tables, random_runs
+def make_plans(group: int, seed: int, plan_blocks: int = PLAN_BLOCKS, runs=None, pair=None):
+    """(out_ops, in_ops): the swap-out of `plan_blocks` in runs of `group`, and
+    the swap-in of exactly those host blocks into another random table.
+    `runs` / `pair` default to paper_2411_18424_b200.synthetic; the reference
+    arm passes the oracle's (identical, tests/test_oracle.py) generators."""
+    if runs is None:
+        from paper_2411_18424_b200.synthetic import pair_tables, random_runs
+        runs, pair = random_runs, pair_tables
     rng = np.random.default_rng(seed)
-    out_ops = random_runs(rng, PLAN_BLOCKS, group, POOL_BLOCKS, HOST_POOL_BLOCKS)
-    in_ops = random_runs(rng, PLAN_BLOCKS, group, POOL_BLOCKS, HOST_POOL_BLOCKS)
-    # swap-in reads back exactly the host blocks swap-out wrote
+    gpu_pool, host_pool = pools(plan_blocks)
+    out_ops = runs(rng, plan_blocks, group, gpu_pool, host_pool)
+    in_ops = runs(rng, plan_blocks, group, gpu_pool, host_pool)
     host_blocks = np.concatenate([np.arange(c, c + b) for b, g, c in out_ops])
     gpu_blocks = np.concatenate([np.arange(g, g + b) for b, g, c in in_ops])
-    in_ops = pair_tables(gpu_blocks, host_blocks)
+    in_ops = pair(gpu_blocks, host_blocks)
     return out_ops.astype(np.int32), in_ops.astype(np.int32)
 
 
-# ------------------------------------------------------------- reference arm
+# ------------------------------------------------------------- CPU baselines
 
-def cpu_oracle_rate(geo, group: int, seconds: float, threads: int):
-    """Oracle C restatement of the same plan shape on host memory (bounded sample)."""
-    from oracle import c_oracle
-    from oracle.bytes_oracle import random_runs
-    sample_blocks = 512  # 1 GiB per direction at 2 MiB blocks
-    pool = 1024
-    rng = np.random.default_rng(1)
-    planes = np.zeros((geo.num_planes, pool, geo.plane_chunk_bytes), dtype=np.uint8)
-    host = np.zeros((pool, geo.block_bytes), dtype=np.uint8)
-    planes[:] = 7
-    ops = random_runs(rng, sample_blocks, min(group, sample_blocks), pool, pool)
-    moved = 0
+class _Timed:
+    """Wrap a bound method; accumulate per-call wall time."""
+
+    def __init__(self, fn):
+        self.fn, self.calls, self.seconds = fn, 0, 0.0
+
+    def __call__(self, *a, **kw):
+        t = time.perf_counter()
+        try:
+            return self.fn(*a, **kw)
+        finally:
+            self.seconds += time.perf_counter() - t
+            self.calls += 1
+
+    def us(self):
+        return round(self.seconds / self.calls * 1e6, 2) if self.calls else None
+
+
+def control_plane_cost(which: str) -> dict:
+    """Per-call cost of the control plane on the bench's stress trace
+    (replay, Markov priorities — the pattern the reference itself accepts):
+    plan_swap_out (cpu_store.py:209), plan_swap_in (cpu_store.py:289),
+    BlockGroupPool.allocate (alloc.py:218), SwapManager.dispatch
+    (swap.py:181) and engine µs per iteration (engine.py:351).
+
+    which="reference": the unmodified reference, installed offline into
+    baseline/_ref; if absent there, says so.  which="ours": this package."""
+    t = TRACES["stress_markov"]
+    doc = {"ablation": "full", "block": {"bytes_per_block": 2097152},
+           "gpu_pool": {"total_blocks": 512}, "cpu_pool": {"total_blocks": t["cpu"]},
+           "workload": {"num_conversations": t["convs"], "arrival_rate_per_s": t["rate"],
+                        "think_time_mean_s": t["think"]},
+           "trace": {"pattern": "markov", "frequency": 0.04}}
+    if which == "reference":
+        ref = ROOT / "baseline" / "_ref"
+        if not (ref / "kvswitch").is_dir():
+            return {"impl": "reference", "unavailable": "baseline/_ref not installed"}
+        if str(ref) not in sys.path:
+            sys.path.insert(0, str(ref))
+        import kvswitch
+        from kvswitch import config as C
+        from kvswitch.engine import Engine as E
+        s = C.build(doc)
+        eng = E(s.engine, kvswitch.generate(s.workload))
+        label = f"reference kvswitch {getattr(kvswitch, '__version__', '0.1.0')} (baseline/_ref)"
+    else:
+        from paper_2411_18424_b200 import config as mconfig
+        from paper_2411_18424_b200.engine import Engine as E
+        from paper_2411_18424_b200.workload import generate
+        cfg, wl, _ = mconfig.build(doc)
+        eng = E(cfg, generate(wl))
+        label = "paper_2411_18424_b200 (this package, replay mode)"
+    hooks = {"plan_swap_out": (eng.store, "plan_swap_out"),
+             "plan_swap_in": (eng.store, "plan_swap_in"),
+             "allocate": (eng.pool, "allocate"), "dispatch": (eng.manager, "dispatch")}
+    timers = {}
+    for name, (obj, attr) in hooks.items():
+        timers[name] = _Timed(getattr(obj, attr))
+        setattr(obj, attr, timers[name])
     t0 = time.perf_counter()
-    reps = 0
+    rep = eng.run()
+    el = time.perf_counter() - t0
+    return {"impl": label, "workload": "bench stress trace (64 conversations, 4 req/s, "
+                                       "think 2 s, 512 x 2 MiB blocks, markov f=0.04), replay",
+            **{f"{k}_us": v.us() for k, v in timers.items()},
+            **{f"{k}_calls": v.calls for k, v in timers.items()},
+            "iter_us": round(el / max(1, rep.iterations) * 1e6, 2),
+            "iterations": rep.iterations, "run_s": round(el, 2)}
+
+
+def cpu_oracle_rate(geo, group: int, seconds: float, threads: int, plan_blocks: int):
+    """The oracle's C restatement moving the bench's own plans (same seed,
+    sizes and pools) between host buffers, on all host threads."""
+    from oracle import c_oracle
+    from oracle.bytes_oracle import random_runs, table_to_ops
+    out_ops, in_ops = make_plans(group, 0, plan_blocks, random_runs, table_to_ops)
+    gpu_pool, host_pool = pools(plan_blocks)
+    planes = np.full((geo.num_planes, gpu_pool, geo.plane_chunk_bytes), 7, dtype=np.uint8)
+    host = np.zeros((host_pool, geo.block_bytes), dtype=np.uint8)
+    nbytes = plan_blocks * geo.block_bytes
+
+    def step():
+        c_oracle.apply_plan_arrays("out", planes, host, out_ops, nthreads=threads)
+        c_oracle.apply_plan_arrays("in", planes, host, in_ops, nthreads=threads)
+
+    step()  # first touch
+    moved, reps = 0, 0
+    t0 = time.perf_counter()
     while True:
-        c_oracle.apply_plan_arrays("out", planes, host, ops, nthreads=threads)
-        c_oracle.apply_plan_arrays("in", planes, host, ops, nthreads=threads)
-        moved += 2 * sample_blocks * geo.block_bytes
+        step()
+        moved += 2 * nbytes
         reps += 1
         el = time.perf_counter() - t0
         if el >= seconds:
             break
-    return moved / el / 1e9, f"{reps} x (swap-out + swap-in) of a {sample_blocks}-block " \
-        f"({sample_blocks * geo.block_bytes >> 20} MiB) plan in runs of {group}, host->host, " \
-        f"{el:.1f} s"
+    return moved / el / 1e9, (f"{reps} x (swap-out + swap-in) of the bench's {plan_blocks}-block "
+                              f"({nbytes >> 20} MiB) plans in runs of {group}, "
+                              f"{gpu_pool}-block 'GPU' and {host_pool}-block host "
+                              f"buffers, {el:.1f} s")
 
 
 def run_reference(args, geo):
@@ -193,16 +347,15 @@ def run_reference(args, geo):
         return  # rank 0 alone runs the CPU reference arm
     threads = os.cpu_count() or 1
     from oracle import c_oracle
-    from oracle.bytes_oracle import random_runs
-    sample_blocks, pool = 512, 1024
-    rng = np.random.default_rng(1)
-    planes = np.full((geo.num_planes, pool, geo.plane_chunk_bytes), 7, dtype=np.uint8)
-    host = np.zeros((pool, geo.block_bytes), dtype=np.uint8)
-    ops = random_runs(rng, sample_blocks, min(args.group, sample_blocks), pool, pool)
+    from oracle.bytes_oracle import random_runs, table_to_ops
+    out_ops, in_ops = make_plans(args.group, 0, args.plan_blocks, random_runs, table_to_ops)
+    gpu_pool, host_pool = pools(args.plan_blocks)
+    planes = np.full((geo.num_planes, gpu_pool, geo.plane_chunk_bytes), 7, dtype=np.uint8)
+    host = np.zeros((host_pool, geo.block_bytes), dtype=np.uint8)
 
     def step():
-        c_oracle.apply_plan_arrays("out", planes, host, ops, nthreads=threads)
-        c_oracle.apply_plan_arrays("in", planes, host, ops, nthreads=threads)
+        c_oracle.apply_plan_arrays("out", planes, host, out_ops, nthreads=threads)
+        c_oracle.apply_plan_arrays("in", planes, host, in_ops, nthreads=threads)
 
     for _ in range(args.warmup):
         step()
@@ -210,25 +363,38 @@ def run_reference(args, geo):
     for _ in range(args.steps):
         step()
     el = time.perf_counter() - t0
-    nbytes = 2 * sample_blocks * geo.block_bytes * args.steps
+    nbytes = 2 * args.plan_blocks * geo.block_bytes * args.steps
     val = nbytes / el / 1e9
-    sample = (f"per step: swap-out + swap-in of a {sample_blocks}-block "
-              f"({sample_blocks * geo.block_bytes >> 20} MiB) plan in runs of {args.group}, "
-              f"host buffers, oracle C restatement, {threads} pthreads")
+    sample = (f"per step: swap-out + swap-in of the bench's {args.plan_blocks}-block "
+              f"({args.plan_blocks * geo.block_bytes >> 20} MiB) plans in runs of {args.group} "
+              f"(same seed and pools as the GPU arm), host buffers, oracle C restatement, "
+              f"{threads} pthreads")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 3), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"config2 block-group swap, {geo.name} KV shape, group={args.group}",
-                   "plan_blocks": sample_blocks, "block_bytes": geo.block_bytes},
-        "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "cores": threads,
-                         "kind": "port", "sample": sample, "cpu_model": cpu_model()},
+        "config": workload_config(args, geo),
+        "cpu_baseline": {"value": round(val, 3), "unit": "GB/s", "kind": "port",
+                         "sample": sample, **host_cpu_info(threads),
+                         "control_plane": control_plane_cost("reference")},
         "e2e": {"value": round(val, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_config(args, geo) -> dict:
+    nb = args.plan_blocks * geo.block_bytes
+    return {"workload": f"config2 block-group swap: {args.plan_blocks}-block plans "
+                        f"({nb / 2**30:g} GiB) out then in, runs of {args.group}, "
+                        f"{geo.name} KV shape",
+            "model_kv": geo.name, "block_bytes": geo.block_bytes,
+            "plan_blocks": args.plan_blocks, "group_blocks": args.group,
+            "gpu_pool_blocks": pools(args.plan_blocks)[0],
+            "host_pool_blocks": pools(args.plan_blocks)[1],
+            "l2": f"inputs {nb / 2**30:g} GiB/direction > 126 MB L2, no flush"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -251,22 +417,41 @@ def run_ours(args, geo):
     dev = torch.device("cuda", local)
     if world > 1:
         if backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
+            try:
+                dist.init_process_group("nccl", device_id=dev)
+            except Exception as exc:  # control-plane agreement works over gloo too
+                print(f"bench: NCCL init failed ({exc}); using gloo", file=sys.stderr)
+                backend = "gloo"
+                dist.init_process_group("gloo")
         else:
             dist.init_process_group(backend)
 
-    cache = PagedKVCache(geo, POOL_BLOCKS, device=dev)
-    host = HostKVPool(HOST_POOL_BLOCKS, geo.block_bytes, numa_node=None, device=dev)
+    gpu_pool, host_pool = pools(args.plan_blocks)
+    cache = PagedKVCache(geo, gpu_pool, device=dev)
+    host = HostKVPool(host_pool, geo.block_bytes, numa_node=None, device=dev)
     host_numa = host.numa_node
+    numa_per_rank, links = [host_numa], [host_link_info(dev)]
+    if world > 1:  # where each rank's swap space lives, and which host link it uses
+        numa_per_rank = [None] * world
+        dist.all_gather_object(numa_per_rank, host_numa)
+        links = [None] * world
+        dist.all_gather_object(links, host_link_info(dev))
     dp = SwapDataPlane(cache, host, ctas={"out": args.ctas, "in": args.ctas})
     cache.planes.view(torch.int32).random_()
-    out_ops, in_ops = make_plans(args.group, seed=rank)
-    nbytes_dir = PLAN_BLOCKS * geo.block_bytes
+    out_ops, in_ops = make_plans(args.group, seed=rank, plan_blocks=args.plan_blocks)
+    nbytes_dir = args.plan_blocks * geo.block_bytes
     s = torch.cuda.Stream(device=dev)
 
     def barrier():
         if world > 1:
             dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     # ---- device-timed steps (KV resident in HBM / host pool) ----
     def step(evs=None):
@@ -299,27 +484,29 @@ def run_ours(args, geo):
     sec = t_start.elapsed_time(t_end) * 1e-3
     out_ms = [e[0].elapsed_time(e[1]) for e in evs]
     in_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    sec_max = sec
-    if world > 1:
-        t = torch.tensor([sec], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sec_max = float(t.item())
+    sec_max = max_over_ranks(sec)
     value = world * 2 * nbytes_dir * args.steps / sec_max / 1e9
     out_gbs = nbytes_dir / (statistics.mean(out_ms) * 1e-3) / 1e9
     in_gbs = nbytes_dir / (statistics.mean(in_ms) * 1e-3) / 1e9
 
     # ---- e2e: public API (control plane + dispatch) with host round trip ----
-    e2e = run_e2e(args, geo, dp, dev, barrier, world)
+    e2e = run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, args.e2e_policy)
+    e2e_serving = run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, "latency")
     dp.set_launch("out", args.ctas, 0)
     dp.set_launch("in", args.ctas, 0)
 
-    # ---- copy-engine peak on this box (roofline context) ----
-    ce = ce_peak(dev, host, cache) if rank == 0 else None
+    # ---- copy-engine peak, all ranks at once (host-link / root-port probe) ----
+    barrier()
+    ce = ce_peak(dev, host, cache)
+    ce_all = [ce]
+    if world > 1:
+        ce_all = [None] * world
+        dist.all_gather_object(ce_all, ce)
 
-    # ---- group-size sweep (config 2), kernel vs copy-engine comparators ----
+    # ---- group-size sweep (config 2): kernel paths vs copy-engine comparators ----
     sweep = None
     if rank == 0 and not args.no_sweep:
-        sweep = group_sweep(dp, s)
+        sweep = group_sweep(dp, s, torch.cuda.Stream(device=dev))
 
     # ---- the SM partition is an optimisation: fall back to shared SMs if the
     #      driver cannot create green contexts on this box ----
@@ -332,56 +519,57 @@ def run_ours(args, geo):
             args.sm_partition = 0
 
     # ---- serving configuration: paced swaps under a concurrent decode load ----
-    serving = serving_interference(dp, dev, s) if rank == 0 else None
-    if rank == 0 and args.sm_partition:
-        serving = {"shared_sms": serving,
-                   f"swap_on_{args.sm_partition}_sms": serving_interference(
-                       dp, dev, s, args.sm_partition)}
+    serving = None
+    if rank == 0:
+        pol = os.environ.get("KVS_SERVING_POLICY", "latency")
+        serving = {"shared_sms": serving_interference(dp, dev, s, 0, pol)}
+        if args.sm_partition:
+            part = f"swap_on_{args.sm_partition}_sms"
+            serving[part] = serving_interference(dp, dev, s, args.sm_partition, pol)
+            serving[part + "_in_share"] = serving_interference(dp, dev, s, args.sm_partition,
+                                                               "latency_share")
 
-    # ---- live multi-turn preemption trace: P99 TTFT / TBT (metric part 2) ----
+    # ---- live multi-turn preemption traces: P99 TTFT / TBT (metric part 2) ----
     trace = None
     if not args.no_trace:
         host.close()  # free the 10 GiB pinned pool before the trace's own pools
-        trace = run_trace(args, geo, dev)
+        trace = {}
+        for name in [t for t in args.traces.split(",") if t]:
+            trace[name] = run_trace(args, geo, dev, name)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        rate, sample = cpu_oracle_rate(geo, args.group, 10.0, threads)
-        cpu = {"value": round(rate, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-               "sample": sample, "cpu_model": cpu_model()}
-
-    numa_per_rank = [host_numa]
-    links = [host_link_info(dev)]
-    if world > 1:  # where each rank's swap space lives, and which host link it uses
-        numa_per_rank = [None] * world
-        dist.all_gather_object(numa_per_rank, host_numa)
-        links = [None] * world
-        dist.all_gather_object(links, host_link_info(dev))
-    root_ports = {l["root_port"] for l in links if l.get("root_port")}
+    root_ports = {lk["root_port"] for lk in links if lk.get("root_port")}
     # Ranks behind one root port share its link: the aggregate roofline is the
     # smaller of one link per rank and one per distinct root port.
     link_cap = PCIE_GEN5_X16_GBS * (min(world, len(root_ports)) if root_ports else world)
+
+    barrier()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        # after every rank's GPU work (the other ranks wait at the barrier below)
+        threads = os.cpu_count() or 1
+        rate, sample = cpu_oracle_rate(geo, args.group, 10.0, threads, args.plan_blocks)
+        cpu = {"value": round(rate, 3), "unit": "GB/s", "kind": "port", "sample": sample,
+               **host_cpu_info(threads),
+               "control_plane": control_plane_cost("reference"),
+               "control_plane_ours": control_plane_cost("ours")}
     if rank == 0:
         dominant, dom_ms = ("in", in_ms) if sum(in_ms) >= sum(out_ms) else ("out", out_ms)
         achieved = nbytes_dir / (statistics.mean(dom_ms) * 1e-3) / 1e9
         traffic = ncu_traffic(dominant)
+        config = workload_config(args, geo)
+        config.update({
+            "parallelism": f"replicas{world} (per-rank KV shard, own PCIe link)",
+            "host_pool": {"blocks": host_pool, "numa_node": host_numa,
+                          "numa_node_per_rank": numa_per_rank, "numa_nodes": numa_nodes()}})
+        ce_sum = {d: round(sum(c[d] for c in ce_all), 3) for d in ("out", "in")}
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(sec_max / args.steps * 1e3, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (random KV bytes, seeded random block tables)",
-            "config": {"workload": f"config2 block-group swap: {PLAN_BLOCKS}-block plans "
-                                   f"({nbytes_dir >> 30} GiB) out then in, runs of {args.group}, "
-                                   f"{geo.name} KV shape",
-                       "model_kv": geo.name, "block_bytes": geo.block_bytes,
-                       "plan_blocks": PLAN_BLOCKS, "group_blocks": args.group,
-                       "parallelism": f"replicas{world} (per-rank KV shard, own PCIe link)",
-                       "l2": "inputs 8 GiB/direction > 126 MB L2, no flush",
-                       "host_pool": {"blocks": HOST_POOL_BLOCKS, "numa_node": host_numa,
-                                     "numa_node_per_rank": numa_per_rank,
-                                     "numa_nodes": numa_nodes()}},
+            "backend": backend if world > 1 else None,
+            "config": config,
             "per_direction_gbs": {"out": round(out_gbs, 3), "in": round(in_gbs, 3)},
             "roofline": {"bound": "pcie", "achieved": round(achieved, 3),
                          "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
@@ -390,7 +578,9 @@ def run_ours(args, geo):
                                        "frac": round(value / (world * PCIE_GEN5_X16_GBS), 4),
                                        "root_ports": len(root_ports) or None,
                                        "topology_cap_gbs": link_cap,
-                                       "frac_of_topology": round(value / link_cap, 4)},
+                                       "frac_of_topology": round(value / link_cap, 4),
+                                       "ce_all_ranks_concurrent_gbs": ce_sum,
+                                       "ce_per_rank_gbs": ce_all},
                          "host_links": links,
                          "kernel": f"kvs_swap_kernel<{dominant}>",
                          "peak_source": "PCIe Gen5 x16 per direction after 128b/130b "
@@ -402,6 +592,7 @@ def run_ours(args, geo):
                                  "peak": measured_hbm_peak(), "unit": "GB/s"},
                          "ncu": ncu_link_rates()},
             "e2e": e2e,
+            "e2e_serving": e2e_serving,
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
@@ -410,42 +601,47 @@ def run_ours(args, geo):
             "trace": trace,
         }
         print(json.dumps(line), flush=True)
+    barrier()
     host.close()
     if world > 1:
         dist.destroy_process_group()
 
 
-def run_e2e(args, geo, dp, dev, barrier, world):
-    """Same bytes through CpuStore + SwapManager.dispatch (the drop-in API)."""
+def run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, policy):
+    """The same bytes through CpuStore + SwapManager.dispatch (the drop-in
+    API), then — untimed — the same round trip with the GPU blocks poisoned
+    between swap-out and swap-in, compared with a snapshot: the leg's bytes
+    are verified, not assumed."""
     import torch
 
-    from paper_2411_18424_b200.synthetic import random_runs
     from paper_2411_18424_b200.costmodel import TransferParams
     from paper_2411_18424_b200.cpu_store import CpuStore
     from paper_2411_18424_b200.swap import StreamExecutor, SwapManager
+    from paper_2411_18424_b200.synthetic import random_runs
 
-    # bulk round trip: the throughput policy (TMA bulk kernels both ways, plan-level waits)
-    ex = StreamExecutor(dp, duplex_policy="throughput")
+    ex = StreamExecutor(dp, duplex_policy=policy)
     mgr = SwapManager(TransferParams(), bytes_per_block=geo.block_bytes, executor=ex)
-    store = CpuStore(HOST_POOL_BLOCKS, reuse_enabled=True)
-    n_req, per = 64, PLAN_BLOCKS // 64
+    gpu_pool, host_pool = pools(args.plan_blocks)
+    store = CpuStore(host_pool, reuse_enabled=True)
+    n_req = 64
+    per = max(1, args.plan_blocks // n_req)
     rng = np.random.default_rng(7)
-    runs = random_runs(rng, PLAN_BLOCKS, args.group, POOL_BLOCKS, HOST_POOL_BLOCKS)
+    runs = random_runs(rng, args.plan_blocks, args.group, gpu_pool, host_pool)
     tables, cursor = [], 0
-    per_runs = per // args.group if per >= args.group else 1
-    for r in range(n_req):
-        ext = [(int(g), int(b)) for b, g, _ in runs[cursor:cursor + per_runs]]
+    per_runs = max(1, per // args.group)
+    for _ in range(n_req):
+        tables.append([(int(g), int(b)) for b, g, _ in runs[cursor:cursor + per_runs]])
         cursor += per_runs
-        tables.append(ext)
     foot = [sum(b for _, b in t) for t in tables]
 
-    def step():
+    def step(poison=None):
         for r in range(n_req):
-            plan = store.plan_swap_out(r, foot[r], tables[r])
-            mgr.dispatch(0, 0, plan)
+            mgr.dispatch(0, 0, store.plan_swap_out(r, foot[r], tables[r]))
+        if poison is not None:
+            ex.synchronize()
+            poison()
         for r in range(n_req):
-            plan = store.plan_swap_in(r, tables[r])
-            mgr.dispatch(0, 0, plan)
+            mgr.dispatch(0, 0, store.plan_swap_in(r, tables[r]))
         ex.synchronize()
         for r in range(n_req):
             store.release(r)
@@ -460,28 +656,46 @@ def run_e2e(args, geo, dp, dev, barrier, world):
     t0 = time.perf_counter()
     for _ in range(args.steps):
         step()
-    el = time.perf_counter() - t0
+    el = max_over_ranks(time.perf_counter() - t0)
     launches = ex.launches - l0
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([el], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el = float(t.item())
+
+    blocks = torch.as_tensor(np.concatenate([np.arange(g, g + b) for t in tables for g, b in t]),
+                             device=dev)
+    planes = dp.cache.planes
+    snap = planes.index_select(1, blocks)
+
+    def poison():
+        planes.index_fill_(1, blocks, 0xFF)
+        torch.cuda.synchronize()  # the executor's streams do not order after torch's
+
+    step(poison)
+    verified = bool(torch.equal(planes.index_select(1, blocks), snap))
+    del snap
+    torch.cuda.empty_cache()
+    if not verified:
+        raise AssertionError(f"e2e ({policy}) round trip bytes differ after swap-in")
     moved = sum(foot) * geo.block_bytes
     for d in ("out", "in"):
         dp.set_path(d, "lsu")
+        dp.set_pace(d, 0.0)
+        dp.set_budget_share(d, 0.0)
+    dp.set_budget(0.0)
+    dp.set_budget_priority(None)
     return {"value": round(world * 2 * moved * args.steps / el / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": moved, "d2h_bytes_per_step": moved,
-            "api": "CpuStore.plan_swap_out/plan_swap_in -> SwapManager.dispatch -> "
-                   "StreamExecutor (throughput policy: TMA bulk kernels) -> kvs_swap (C ABI); "
-                   "wall clock incl. planning and sync",
-            "requests_per_step": n_req, "gpu_launches": launches}
+            "policy": policy,
+            "api": f"CpuStore.plan_swap_out/plan_swap_in -> SwapManager.dispatch -> "
+                   f"StreamExecutor ({policy} policy) -> kvs_swap (C ABI); "
+                   f"wall clock incl. planning and sync",
+            "requests_per_step": n_req, "gpu_launches": launches,
+            "bytes_verified": verified}
 
 
-def run_trace(args, geo, dev):
+def run_trace(args, geo, dev, name):
     """Live-mode multi-turn preemption trace on this GPU (paper_2411_18424_b200.live):
-    FastSwitch (block groups + reuse + adaptive async, one kernel per plan) vs the
-    vLLM-style baseline (per-block copies on the copy engines)."""
+    FastSwitch (block groups + reuse + adaptive async + layered admission, one
+    kernel per plan) vs the vLLM-style baseline (per-block copies on the copy
+    engines), on the same conversations and priorities."""
     import dataclasses
 
     from paper_2411_18424_b200 import config as mconfig
@@ -489,6 +703,9 @@ def run_trace(args, geo, dev):
     from paper_2411_18424_b200.runtime import Runtime
     from paper_2411_18424_b200.workload import generate
 
+    t = dict(TRACES[name])
+    if args.trace_convs:
+        t["convs"] = args.trace_convs
     _, world, _ = dist_env()
     agreement = None
     if world > 1:
@@ -503,18 +720,18 @@ def run_trace(args, geo, dev):
         ctas = 2 * sms[1]
     decode = DecodeEmulator(dev, weight_bytes=16 << 30, ctas=ctas, stream=stream)
     doc = {"block": {"bytes_per_block": geo.block_bytes}, "gpu_pool": {"total_blocks": 512},
-           "cpu_pool": {"total_blocks": 4096},
-           "workload": {"num_conversations": args.trace_convs, "arrival_rate_per_s": 4.0,
-                        "think_time_mean_s": 2.0},
-           "trace": {"pattern": args.trace_pattern, "frequency": 0.04}}
-    out = {"workload": f"{args.trace_convs} conversations, 4 req/s, think 2 s, 512 x "
-                       f"{geo.block_bytes / 2**20:g} MiB GPU blocks per rank (TP{world}), "
-                       f"{args.trace_pattern} priorities f=0.04 (BASELINE config 3: VTC), "
-                       f"decode = {decode.bytes_per_us / 1e3:.0f} GB/s weight "
-                       f"streaming per rank",
-           "tp": world, "sm_partition": sms, "runs": {}}
-    for name, mode, impl in (("fastswitch", "full", "kernel"),
-                             ("vllm_like", "baseline", "ce_per_block")):
+           "cpu_pool": {"total_blocks": t["cpu"]},
+           "workload": {"num_conversations": t["convs"], "arrival_rate_per_s": t["rate"],
+                        "think_time_mean_s": t["think"]},
+           "trace": {"pattern": t["pattern"], "frequency": 0.04}}
+    out = {"workload": f"{t['convs']} conversations, {t['rate']:g} req/s, think "
+                       f"{t['think']:g} s, 512 x {geo.block_bytes / 2**20:g} MiB GPU blocks "
+                       f"per rank (TP{world}), {t['cpu']}-block host pool, {t['pattern']} "
+                       f"priorities f=0.04, decode = {decode.bytes_per_us / 1e3:.0f} GB/s "
+                       f"weight streaming per rank + KV reads of every resident token",
+           "pattern": t["pattern"], "tp": world, "sm_partition": sms, "runs": {}}
+    for run, mode, impl in (("fastswitch", "full", "kernel"),
+                            ("vllm_like", "baseline", "ce_per_block")):
         cfg, wl, _ = mconfig.build({**doc, "ablation": mode})
         cfg = dataclasses.replace(cfg, transfer=b200_transfer_params())
         layered = impl == "kernel" and not args.no_layered
@@ -527,35 +744,38 @@ def run_trace(args, geo, dev):
         lat = eng.latency_summary()
         anat = eng.ttft_anatomy()
         st = rt.stats()
-        out["runs"][name] = {"ablation": mode, "copy_impl": impl,
-                             **{k: lat[k] for k in ("ttft_p50_ms", "ttft_p99_ms", "tbt_p99_ms",
-                                                    "tbt_p999_ms", "decode_stall_frac",
-                                                    "swap_induced_decode_stall", "wall_s")},
-                             "ttft_tail_ms": {"turns": anat.get("turns"),
-                                              **anat.get("tail_mean_ms", {})},
-                             "layered_joins": lat["layered_joins"],
-                             "kv_read_gib_verified": lat["kv_read_gib"],
-                             "tokens": rep.total_tokens,
-                             "swap_gib": {"out": round(st["bytes_out"] / 2**30, 2),
-                                          "in": round(st["bytes_in"] / 2**30, 2)},
-                             "kernel_launches": st["kernel_launches"]}
+        out["runs"][run] = {"ablation": mode, "copy_impl": impl,
+                            **{k: lat[k] for k in ("ttft_p50_ms", "ttft_p95_ms", "ttft_p99_ms",
+                                                   "tbt_p50_ms", "tbt_p99_ms", "tbt_p999_ms",
+                                                   "decode_stall_frac",
+                                                   "swap_induced_decode_stall", "stall_model",
+                                                   "solo_decode_ms", "solo_decode_drift",
+                                                   "wall_s")},
+                            "ttft_tail_ms": {"turns": anat.get("turns"),
+                                             **anat.get("tail_mean_ms", {})},
+                            "layered_joins": lat["layered_joins"],
+                            "kv_read_gib_verified": lat["kv_read_gib"],
+                            "tokens": rep.total_tokens,
+                            "swap_gib": {"out": round(st["bytes_out"] / 2**30, 2),
+                                         "in": round(st["bytes_in"] / 2**30, 2)},
+                            "swap_rates": rt.swap_rates(),
+                            "kernel_launches": st["kernel_launches"]}
         rt.close()
     del decode
     torch_empty_cache()
     return out
 
 
-def serving_interference(dp, dev, s, sm_partition: int = 0):
+def serving_interference(dp, dev, s, sm_partition: int = 0, policy: str = "latency"):
     """Swap-induced decode stall, measured: 2 ms HBM-streaming decode steps on a
-    high-priority stream while a 2 GiB swap runs, per direction, with the
-    serving ("latency") policy: paced kernels + shared budget (swap.py)."""
-    import statistics
-
+    high-priority stream while a 2 GiB swap runs, per direction and both at
+    once, under a serving policy (swap.DUPLEX_POLICIES: paced kernels, shared
+    budget, optional reserved share)."""
     import torch
 
-    from paper_2411_18424_b200.synthetic import random_runs
     from paper_2411_18424_b200.live import DecodeEmulator
     from paper_2411_18424_b200.swap import DUPLEX_POLICIES
+    from paper_2411_18424_b200.synthetic import random_runs
 
     if sm_partition:
         from paper_2411_18424_b200.swap import partition_streams
@@ -567,11 +787,12 @@ def serving_interference(dp, dev, s, sm_partition: int = 0):
         comp = torch.cuda.Stream(device=dev, priority=-1)
         s2 = torch.cuda.Stream(device=dev)
     rng = np.random.default_rng(5)
-    n = 1024
-    ops = random_runs(rng, n, 16, POOL_BLOCKS // 2, HOST_POOL_BLOCKS // 2).astype(np.int32)
+    gp, hp = dp.cache.num_blocks // 2, dp.host.num_blocks // 2
+    n = min(1024, hp // 2)
+    ops = random_runs(rng, n, 16, gp, hp).astype(np.int32)
     ops_in = ops.copy()
-    ops_in[:, 1] += POOL_BLOCKS // 2
-    ops_in[:, 2] += HOST_POOL_BLOCKS // 2
+    ops_in[:, 1] += gp
+    ops_in[:, 2] += hp
     nbytes = n * dp.geometry.block_bytes
 
     def steps(k):
@@ -587,12 +808,13 @@ def serving_interference(dp, dev, s, sm_partition: int = 0):
     ev = steps(20)
     torch.cuda.synchronize()
     solo = statistics.median(ev[i].elapsed_time(ev[i + 1]) for i in range(20))
-    policy = os.environ.get("KVS_SERVING_POLICY", "latency")
     pol = DUPLEX_POLICIES[policy]
     for d in ("out", "in"):
         c, t, pace = pol[d]
+        dp.set_path(d, pol.get("path", "lsu"))
         dp.set_launch(d, c, t)
         dp.set_pace(d, pace)
+        dp.set_budget_share(d, pol.get("share", {}).get(d, 0.0))
     dp.set_budget(pol["budget"])
     dp.set_budget_priority(pol.get("priority"))
     out = {"policy": policy, "sm_partition": sms, "decode_step_solo_ms": round(solo, 3),
@@ -618,8 +840,10 @@ def serving_interference(dp, dev, s, sm_partition: int = 0):
             "decode_steps": len(st_ms),
             "decode_slowdown": round(statistics.median(st_ms) / solo - 1, 4) if st_ms else None}
     for d in ("out", "in"):
+        dp.set_path(d, "lsu")
         dp.set_launch(d, 0, 0)
         dp.set_pace(d, 0.0)
+        dp.set_budget_share(d, 0.0)
     dp.set_budget(0.0)
     dp.set_budget_priority(None)
     del dec
@@ -654,30 +878,74 @@ def ce_peak(dev, host, cache):
     return res
 
 
-def group_sweep(dp, s):
+SWEEP_ENGINES = ("kernel_lsu", "kernel_bulk", "ce_per_block", "ce_per_run", "ce_batch")
+
+
+def group_sweep(dp, s, s2):
+    """Config 2: swap GB/s vs group size for every engine —
+    K1/K2 LSU (v1) and TMA bulk (v2), K3 per-block (vLLM swap_blocks, the
+    reference's split_single path, swap.py:170-179), K3 per-run (one 2D copy
+    per run), K4 cudaMemcpyBatchAsync — per direction (a 4096-block plan) and
+    both directions at once (2048-block plans each way on disjoint halves of
+    the pools; combined GB/s over the union of both streams' lifetimes)."""
     import torch
+
     from paper_2411_18424_b200.synthetic import random_runs
     geo = dp.geometry
-    out = []
+    gp, hp = dp.cache.num_blocks, dp.host.num_blocks
+    plan = min(PLAN_BLOCKS, hp // 2)
+    nbytes = plan * geo.block_bytes
     rng = np.random.default_rng(11)
-    nbytes = PLAN_BLOCKS * geo.block_bytes
-    for g in (1, 4, 16, 64, 256):
-        ops = random_runs(rng, PLAN_BLOCKS, g, POOL_BLOCKS, HOST_POOL_BLOCKS).astype(np.int32)
-        row = {"group": g}
+
+    def launch(engine, d, ops, stream):
+        if engine.startswith("kernel"):
+            dp.set_path(d, "bulk" if engine == "kernel_bulk" else "lsu")
+            dp.swap(d, ops, stream=stream)
+        else:
+            dp.baseline(d, ("ce_per_block", "ce_per_run", "ce_batch").index(engine), ops,
+                        stream=stream)
+
+    def timed(fn_by_stream):
+        torch.cuda.synchronize()
+        marks = []
+        for st, fn in fn_by_stream:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            fn()
+            e1.record(st)
+            marks.append((e0, e1))
+        torch.cuda.synchronize()
+        ref = marks[0][0]
+        lo = min(ref.elapsed_time(a) for a, _ in marks)
+        hi = max(ref.elapsed_time(b) for _, b in marks)
+        return (hi - lo) * 1e-3
+
+    warm = random_runs(rng, min(256, plan), 16, gp, hp).astype(np.int32)
+    for e in SWEEP_ENGINES:  # first use of every path outside the timed calls
         for d in ("out", "in"):
-            for impl, fn in (("kernel", lambda: dp.swap(d, ops, stream=s)),
-                             ("ce_per_run", lambda: dp.baseline(d, 1, ops, stream=s)),
-                             ("ce_batch", lambda: dp.baseline(d, 2, ops, stream=s))):
-                fn()
-                s.synchronize()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(s)
-                fn()
-                e1.record(s)
-                s.synchronize()
-                row[f"{d}_{impl}"] = round(nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9, 2)
-        out.append(row)
-    return out
+            launch(e, d, warm, s)
+    torch.cuda.synchronize()
+    rows = []
+    for g in SWEEP_GROUPS:
+        ops = random_runs(rng, plan, g, gp, hp).astype(np.int32)
+        half = plan // 2
+        h_out = random_runs(rng, half, g, gp // 2, hp // 2).astype(np.int32)
+        h_in = random_runs(rng, half, g, gp // 2, hp // 2).astype(np.int32)
+        h_in[:, 1] += gp // 2
+        h_in[:, 2] += hp // 2
+        row = {"group": g, "ops": int(len(ops))}
+        for e in SWEEP_ENGINES:
+            for d in ("out", "in"):
+                sec = timed([(s, lambda: launch(e, d, ops, s))])
+                row[f"{d}_{e}"] = round(nbytes / sec / 1e9, 2)
+            sec = timed([(s, lambda: launch(e, "out", h_out, s)),
+                         (s2, lambda: launch(e, "in", h_in, s2))])
+            row[f"duplex_{e}"] = round(2 * half * geo.block_bytes / sec / 1e9, 2)
+        rows.append(row)
+    for d in ("out", "in"):
+        dp.set_path(d, "lsu")
+    return {"plan_blocks": plan, "block_bytes": geo.block_bytes, "engines": SWEEP_ENGINES,
+            "unit": "GB/s", "rows": rows}
 
 
 def measured_hbm_peak():
@@ -712,6 +980,7 @@ def ncu_link_rates():
 
 def main():
     args = parse()
+    relaunch_if_needed(args)
     from paper_2411_18424_b200.geometry import PRESETS
     geo = PRESETS[args.model]
     if args.impl == "reference":

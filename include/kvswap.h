@@ -102,9 +102,11 @@ int kvs_set_launch(KvsHandle* h, int dir, int ctas, int threads);
 
 /* Select the kernel path for one direction.  piece_bytes / stages tune the
  * bulk path's smem ring (0 = defaults: 16 KiB x 4); ignored by the LSU path.
- * The bulk path serves kvs_swap (whole-plan done flag); kvs_swap_ops,
- * kvs_swap_layered and kvs_swap_signaled always run the LSU kernel, whose
- * warps credit per-op / per-plane counters. */
+ * Both paths serve every entry point and publish every completion word:
+ * LSU warps credit per-op / per-plane counters lazily (one system fence per
+ * warp and op / plane group); the bulk path's elected thread credits on its
+ * store side once the TMA stores it issued for an op / group completed
+ * (cp.async.bulk.wait_group 0, then a system fence). */
 int kvs_set_path(KvsHandle* h, int dir, int path, int piece_bytes, int stages);
 
 /* Pace one direction's LSU kernel to `gbps` GB/s (0 = unpaced).  Stores to
@@ -126,6 +128,15 @@ int kvs_set_budget(KvsHandle* h, double gbps);
  * (engine.py:376-384), while a swap-out's freed blocks are merely busy
  * (engine.py:609, conflicts resolved per op). */
 int kvs_set_budget_priority(KvsHandle* h, int dir);
+
+/* Reserved share of the shared budget: direction `dir` always gets at least
+ * `gbps` GB/s (0 = none) - a piece goes at the earlier of its shared-budget
+ * slot and its slot on a private clock at `gbps` - while its pieces still
+ * charge the shared budget, so a saturating other direction gets the budget
+ * minus the reservation.  Between FCFS (no share) and strict priority
+ * (kvs_set_budget_priority): a resume is not starved by a burst of
+ * preemptions, nor does it starve them (engine.py:376-384 vs :591-611). */
+int kvs_set_budget_share(KvsHandle* h, int dir, double gbps);
 
 /* STREAM RULE — kvs_swap, kvs_swap_ops, kvs_swap_layered, kvs_swap_signaled:
  * completion words are published through per-handle, per-direction device

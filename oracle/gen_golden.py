@@ -61,7 +61,7 @@ ENGINE_CASES = {
                      "trace": {"pattern": "markov", "frequency": 0.04}},
     # BASELINE config 3: VTC priorities (reference engine + oracle/vtc_oracle.py)
     "vtc_config3_bench": {"ablation": "full", "block": {"bytes_per_block": 2097152},
-                          "gpu_pool": {"total_blocks": 512},
+                          "gpu_pool": {"total_blocks": 512}, "cpu_pool": {"total_blocks": 4096},
                           "workload": {"num_conversations": 64, "arrival_rate_per_s": 4.0,
                                        "think_time_mean_s": 2.0},
                           "trace": {"pattern": "vtc", "frequency": 0.04}},
@@ -72,6 +72,7 @@ ENGINE_CASES = {
                             "trace": {"pattern": "vtc", "frequency": 0.04}},
     "vtc_config3_baseline": {"ablation": "baseline", "block": {"bytes_per_block": 2097152},
                              "gpu_pool": {"total_blocks": 512},
+                             "cpu_pool": {"total_blocks": 4096},
                              "workload": {"num_conversations": 64, "arrival_rate_per_s": 4.0,
                                           "think_time_mean_s": 2.0},
                              "trace": {"pattern": "vtc", "frequency": 0.04}},

@@ -49,6 +49,7 @@ EXPORTED_SYMBOLS = (
     "kvs_set_pace",
     "kvs_set_budget",
     "kvs_set_budget_priority",
+    "kvs_set_budget_share",
     "kvs_swap",
     "kvs_swap_layered",
     "kvs_set_layer_group",
@@ -120,6 +121,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_set_budget.argtypes = [c.c_void_p, c.c_double]
     lib.kvs_set_budget_priority.restype = c.c_int
     lib.kvs_set_budget_priority.argtypes = [c.c_void_p, c.c_int]
+    lib.kvs_set_budget_share.restype = c.c_int
+    lib.kvs_set_budget_share.argtypes = [c.c_void_p, c.c_int, c.c_double]
     lib.kvs_set_layer_group.restype = c.c_int
     lib.kvs_set_layer_group.argtypes = [c.c_void_p, c.c_int]
     lib.kvs_swap.restype = c.c_int

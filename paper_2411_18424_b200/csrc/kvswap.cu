@@ -73,6 +73,8 @@ struct SwapParams {
   uint64_t bucket_cost_ns;     // >0: ns of budget one piece consumes
   uint64_t bucket_burst_ns;    // idle credit cap
   uint32_t bucket_nowait;      // 1: charge the shared budget but never wait (priority side)
+  unsigned long long* share;   // this direction's reserved-rate clock, ns
+  uint64_t share_cost_ns;      // >0: a piece may also go on this direction's reservation
   int32_t op_end[CAP];         // inclusive prefix sum of TransferOp.blocks
   int32_t op_gpu[CAP];         // TransferOp.gpu_start
   int32_t op_cpu[CAP];         // TransferOp.cpu_start
@@ -106,6 +108,22 @@ __device__ __forceinline__ unsigned long long take_budget(unsigned long long* bu
   return atomicAdd(bucket, static_cast<unsigned long long>(cost));
 }
 
+// Budget slot of one piece: the shared clock, or - when this direction holds
+// a reserved share of the budget - the earlier of the shared slot and the
+// slot on its own reserved-rate clock.  Both clocks are charged, so the
+// reserved traffic still counts against the budget the other direction sees:
+// with swap-in reserving R of a budget B, a saturating swap-out gets B - R
+// while swap-in always gets at least R.
+template <typename P>
+__device__ __forceinline__ unsigned long long budget_slot(const P& p) {
+  unsigned long long slot = take_budget(p.bucket, p.bucket_cost_ns, p.bucket_burst_ns);
+  if (p.share_cost_ns != 0) {
+    const unsigned long long own = take_budget(p.share, p.share_cost_ns, 16 * p.share_cost_ns);
+    slot = own < slot ? own : slot;
+  }
+  return slot;
+}
+
 // Release fence at system scope: this thread's (and, after __syncwarp, its
 // warp's) prior writes - host-mapped ones included - are ordered before what
 // it writes next.  acq_rel is all the credit / publish protocol needs; the
@@ -119,32 +137,47 @@ __device__ __forceinline__ void publish(uint32_t* flag, uint32_t seq) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
 }
 
-// Add a warp's `n` finished pieces of plane group `grp` to the group's
-// counter; the warp that completes the group publishes seq for every plane
-// of it.  Warp-uniform call.
+// Add `n` finished (and fenced) pieces of plane group `grp` to the group's
+// counter; the caller that completes the group publishes seq for every plane
+// of it.  One thread.
+template <int CAP>
+__device__ __forceinline__ void credit_group_1(const SwapParams<CAP>& p, uint32_t grp,
+                                               uint32_t n) {
+  const uint32_t first = grp * p.layer_group;
+  const uint32_t g_here = min(p.layer_group, p.num_planes - first);
+  const unsigned long long want = static_cast<unsigned long long>(p.pieces_per_plane) * g_here;
+  const unsigned long long old = atomicAdd(p.plane_ctr + grp, static_cast<unsigned long long>(n));
+  if (old + n == want) {
+    // Every piece of the group is counted: publish, and leave the counter
+    // at zero for the next launch of this direction (no memset node).
+    p.plane_ctr[grp] = 0;
+    for (uint32_t l = 0; l < g_here; ++l) publish(p.plane_flags + first + l, p.seq);
+  }
+}
+
+// Same for a TransferOp (`want` = all its pieces across planes).  One thread.
+template <int CAP>
+__device__ __forceinline__ void credit_op_1(const SwapParams<CAP>& p, int op, uint32_t n,
+                                            uint32_t want) {
+  if (atomicAdd(p.op_ctr + op, n) + n == want) {
+    p.op_ctr[op] = 0;  // counted in full: reset for the next launch
+    publish(p.op_flags + op, p.seq);
+  }
+}
+
+// Warp-uniform wrappers for the LSU kernel: every lane's stores precede lane
+// 0's system fence, then lane 0 credits.
 template <int CAP>
 __device__ __forceinline__ void credit_group(const SwapParams<CAP>& p, uint32_t lane,
                                              uint32_t grp, uint32_t n) {
   if (p.plane_flags == nullptr || n == 0) return;
-  __syncwarp();  // every lane's stores precede lane 0's fence
+  __syncwarp();
   if (lane == 0) {
     fence_sys();
-    const uint32_t first = grp * p.layer_group;
-    const uint32_t g_here = min(p.layer_group, p.num_planes - first);
-    const unsigned long long want =
-        static_cast<unsigned long long>(p.pieces_per_plane) * g_here;
-    const unsigned long long old =
-        atomicAdd(p.plane_ctr + grp, static_cast<unsigned long long>(n));
-    if (old + n == want) {
-      // Every piece of the group is counted: publish, and leave the counter
-      // at zero for the next launch of this direction (no memset node).
-      p.plane_ctr[grp] = 0;
-      for (uint32_t l = 0; l < g_here; ++l) publish(p.plane_flags + first + l, p.seq);
-    }
+    credit_group_1(p, grp, n);
   }
 }
 
-// Same for a TransferOp (`want` = all its pieces across planes).
 template <int CAP>
 __device__ __forceinline__ void credit_op(const SwapParams<CAP>& p, uint32_t lane, int op,
                                           uint32_t n, uint32_t want) {
@@ -152,10 +185,50 @@ __device__ __forceinline__ void credit_op(const SwapParams<CAP>& p, uint32_t lan
   __syncwarp();
   if (lane == 0) {
     fence_sys();
-    if (atomicAdd(p.op_ctr + op, n) + n == want) {
-      p.op_ctr[op] = 0;  // counted in full: reset for the next launch
-      publish(p.op_flags + op, p.seq);
-    }
+    credit_op_1(p, op, n, want);
+  }
+}
+
+// Plan piece i -> (plan-order block k, plane, piece within the chunk).
+// Block-major: all planes of block 0, then block 1, ...  Layered: plane-major
+// in groups of layer_group planes (every block of planes [0, g), then of
+// [g, 2g), ...), block-major inside a group, so layer l's KV lands (and is
+// flagged) before later groups' while host reads stay g x chunk contiguous
+// (SURVEY §8f rank 2).
+template <int CAP>
+__device__ __forceinline__ void piece_coords(const SwapParams<CAP>& p, uint32_t i, uint32_t& k,
+                                             uint32_t& plane, uint32_t& piece) {
+  if (p.layered) {
+    const uint32_t g = p.layer_group;
+    const uint32_t per_group = p.pieces_per_plane * g;
+    const uint32_t group = i / per_group;
+    const uint32_t j = i - group * per_group;
+    const uint32_t g_here = min(g, p.num_planes - group * g);
+    const uint32_t chunk_idx = j / p.pieces_per_chunk;
+    piece = j - chunk_idx * p.pieces_per_chunk;
+    k = chunk_idx / g_here;
+    plane = group * g + (chunk_idx - k * g_here);
+  } else {
+    const uint32_t chunk_idx = i / p.pieces_per_chunk;
+    piece = i - chunk_idx * p.pieces_per_chunk;
+    k = chunk_idx / p.num_planes;
+    plane = chunk_idx - k * p.num_planes;
+  }
+}
+
+// Move an op cursor to the TransferOp holding plan block k.  A thread's
+// pieces move forward, so the cursor only advances - except across plane
+// groups in layered order, where block numbering restarts: rewind then.
+template <int CAP>
+__device__ __forceinline__ void op_seek(const SwapParams<CAP>& p, uint32_t k, int& op,
+                                        int32_t& op_begin) {
+  if (static_cast<int32_t>(k) < op_begin) {
+    op = 0;
+    op_begin = 0;
+  }
+  while (static_cast<int32_t>(k) >= p.op_end[op]) {
+    op_begin = p.op_end[op];
+    ++op;
   }
 }
 
@@ -179,35 +252,8 @@ __global__ void __launch_bounds__(kMaxThreads)
   uint32_t acc_op_n = 0, acc_op_want = 0;  // uncredited pieces of acc_op, its total
   for (uint32_t i = warp; i < p.total_pieces; i += nwarps) {
     uint32_t k, plane, piece;
-    if (p.layered) {
-      // Plane-major in groups of layer_group planes: every block of planes
-      // [0, g), then of [g, 2g), ... so layer l's KV lands (and is flagged)
-      // before later groups'.  Within a group the order
-      // is block-major, so the host side still reads g x chunk contiguous.
-      const uint32_t g = p.layer_group;
-      const uint32_t per_group = p.pieces_per_plane * g;
-      const uint32_t group = i / per_group;
-      const uint32_t j = i - group * per_group;
-      const uint32_t g_here = min(g, p.num_planes - group * g);
-      const uint32_t chunk_idx = j / p.pieces_per_chunk;
-      piece = j - chunk_idx * p.pieces_per_chunk;
-      k = chunk_idx / g_here;
-      plane = group * g + (chunk_idx - k * g_here);
-      if (static_cast<int32_t>(k) < op_begin) {  // next group: rewind the cursor
-        op = 0;
-        op_begin = 0;
-      }
-    } else {
-      const uint32_t chunk_idx = i / p.pieces_per_chunk;
-      piece = i - chunk_idx * p.pieces_per_chunk;
-      k = chunk_idx / p.num_planes;  // plan-order block
-      plane = chunk_idx - k * p.num_planes;
-    }
-    // Pieces only move forward for a warp, so the op cursor only advances.
-    while (static_cast<int32_t>(k) >= p.op_end[op]) {
-      op_begin = p.op_end[op];
-      ++op;
-    }
+    piece_coords(p, i, k, plane, piece);
+    op_seek(p, k, op, op_begin);
     if (p.pace_ps != 0) {
       // Rate pacing: posted sysmem stores (and, less so, non-posted reads)
       // issued faster than PCIe drains them back up the XBAR/L2 queues the
@@ -220,7 +266,7 @@ __global__ void __launch_bounds__(kMaxThreads)
       // under one rate, whatever their mix (a token bucket on a global clock).
       // The priority direction only charges it; the other one waits its turn.
       unsigned long long slot = 0;
-      if (lane == 0) slot = take_budget(p.bucket, p.bucket_cost_ns, p.bucket_burst_ns);
+      if (lane == 0) slot = budget_slot(p);
       slot = __shfl_sync(0xffffffffu, slot, 0);
       if (!p.bucket_nowait)
         while (globaltimer_ns() < slot) __nanosleep(64);
@@ -363,18 +409,15 @@ __device__ __forceinline__ void bulk_wait_all() {
 
 constexpr int kMaxStages = 16;
 
-// Resolve piece `i` of the plan into (src, dst, bytes) for direction DIR.
+// Resolve piece `i` of the plan into (src, dst, bytes) for direction DIR;
+// `plane` receives the piece's plane (completion tracking).
 template <int DIR, int CAP>
 __device__ __forceinline__ uint32_t bulk_piece(const SwapParams<CAP>& p, uint32_t i, int& op,
-                                               int32_t& op_begin, const char*& src, char*& dst) {
-  const uint32_t chunk_idx = i / p.pieces_per_chunk;
-  const uint32_t piece = i - chunk_idx * p.pieces_per_chunk;
-  const uint32_t k = chunk_idx / p.num_planes;
-  const uint32_t plane = chunk_idx - k * p.num_planes;
-  while (static_cast<int32_t>(k) >= p.op_end[op]) {
-    op_begin = p.op_end[op];
-    ++op;
-  }
+                                               int32_t& op_begin, const char*& src, char*& dst,
+                                               uint32_t& plane) {
+  uint32_t k, piece;
+  piece_coords(p, i, k, plane, piece);
+  op_seek(p, k, op, op_begin);
   const int64_t rel = static_cast<int64_t>(k) - op_begin;
   const int64_t off = static_cast<int64_t>(piece) * p.piece_bytes;
   char* gpu = reinterpret_cast<char*>(p.planes[plane]) + (p.op_gpu[op] + rel) * p.stride + off;
@@ -390,6 +433,9 @@ template <int DIR, int CAP>
 __global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant__ SwapParams<CAP> p) {
   extern __shared__ __align__(128) char ring[];
   __shared__ __align__(8) uint64_t bars[kMaxStages];
+  const bool ops_at_end = p.layered && p.op_flags != nullptr;
+  const bool op_per_cta = p.op_flags != nullptr && !ops_at_end;
+  const bool tracking = p.plane_flags != nullptr || op_per_cta;
   if (threadIdx.x == 0) {
     const uint32_t S = p.stages;
     for (uint32_t s = 0; s < S; ++s) mbar_init(&bars[s], 1);
@@ -401,6 +447,21 @@ __global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant
     int lop = 0, sop = 0;          // op cursors: loads run ahead of stores
     int32_t lbeg = 0, sbeg = 0;
     uint32_t phase_bits = 0;
+    // Completion tracking on the store side, credited lazily like the LSU
+    // path: when the store cursor moves to another op / plane group, wait
+    // for this CTA's stores so far to complete, fence, and add their count.
+    uint32_t acc_grp = 0xFFFFFFFFu, acc_grp_n = 0;
+    int acc_op = -1;
+    uint32_t acc_op_n = 0, acc_op_want = 0;
+    auto flush = [&]() {
+      if (acc_grp_n == 0 && acc_op_n == 0) return;
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // async-proxy stores done
+      fence_sys();
+      if (p.plane_flags != nullptr && acc_grp_n) credit_group_1(p, acc_grp, acc_grp_n);
+      if (op_per_cta && acc_op_n) credit_op_1(p, acc_op, acc_op_n, acc_op_want);
+      acc_grp_n = acc_op_n = 0;
+    };
     const uint64_t t0 = p.pace_ps != 0 ? globaltimer_ns() : 0;
     // Pacing (kvs_set_pace): piece i's load may not issue before t0 + i*pace.
     auto pace = [&](uint32_t i) {
@@ -409,18 +470,18 @@ __global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant
         while (globaltimer_ns() < due) __nanosleep(64);
       }
       if (p.bucket_cost_ns != 0) {
-        const unsigned long long slot = take_budget(p.bucket, p.bucket_cost_ns,
-                                                    p.bucket_burst_ns);
+        const unsigned long long slot = budget_slot(p);
         if (!p.bucket_nowait)
           while (globaltimer_ns() < slot) __nanosleep(64);
       }
     };
+    uint32_t plane;
     const uint32_t pre = n < S - 1 ? n : S - 1;
     for (uint32_t j = 0; j < pre; ++j) {
       const char* src;
       char* dst;
       pace(first + j * gridDim.x);
-      const uint32_t b = bulk_piece<DIR>(p, first + j * gridDim.x, lop, lbeg, src, dst);
+      const uint32_t b = bulk_piece<DIR>(p, first + j * gridDim.x, lop, lbeg, src, dst, plane);
       mbar_expect_tx(&bars[j % S], b);
       bulk_load(ring + (j % S) * p.piece_bytes, src, b, &bars[j % S]);
     }
@@ -428,34 +489,55 @@ __global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant
       const uint32_t slot = j % S;
       const char* src;
       char* dst;
-      const uint32_t b = bulk_piece<DIR>(p, first + j * gridDim.x, sop, sbeg, src, dst);
+      const uint32_t b = bulk_piece<DIR>(p, first + j * gridDim.x, sop, sbeg, src, dst, plane);
+      if (tracking) {
+        const uint32_t grp = plane / p.layer_group;
+        if ((p.plane_flags != nullptr && grp != acc_grp) || (op_per_cta && sop != acc_op)) {
+          flush();
+          acc_grp = grp;
+          acc_op = sop;
+          acc_op_want = static_cast<uint32_t>(p.op_end[sop] - sbeg) * p.num_planes *
+                        p.pieces_per_chunk;
+        }
+      }
       mbar_wait(&bars[slot], (phase_bits >> slot) & 1u);
       phase_bits ^= 1u << slot;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       bulk_store(dst, ring + slot * p.piece_bytes, b);
+      ++acc_grp_n;
+      ++acc_op_n;
       const uint32_t jj = j + S - 1;
       if (jj < n) {
         // slot jj % S was last read by store j-1: allow only store j in flight.
         bulk_wait_read<1>();
         const char* s2;
         char* d2;
+        uint32_t plane2;
         pace(first + jj * gridDim.x);
-        const uint32_t b2 = bulk_piece<DIR>(p, first + jj * gridDim.x, lop, lbeg, s2, d2);
+        const uint32_t b2 =
+            bulk_piece<DIR>(p, first + jj * gridDim.x, lop, lbeg, s2, d2, plane2);
         mbar_expect_tx(&bars[jj % S], b2);
         bulk_load(ring + (jj % S) * p.piece_bytes, s2, b2, &bars[jj % S]);
       }
     }
+    if (tracking) flush();
     bulk_wait_all();
   }
-  if (p.done_flag != nullptr) {
+  if (p.done_flag != nullptr || ops_at_end) {
+    // As in the LSU kernel: the last CTA to retire publishes the plan-end
+    // words (in plane-major order a TransferOp completes with its last plane).
     __syncthreads();
     if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
       __threadfence_system();
       const unsigned long long t = atomicAdd(p.ticket, 1ull);
       if (t == p.ticket_base + gridDim.x - 1) {
         __threadfence_system();
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.seq)
-                     : "memory");
+        if (ops_at_end)
+          for (int32_t i = 0; i < p.n_ops; ++i) publish(p.op_flags + i, p.seq);
+        if (p.done_flag != nullptr)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.seq)
+                       : "memory");
       }
     }
   }
@@ -483,6 +565,7 @@ struct KvsHandle {
   uint64_t pace_ps[2] = {0, 0};  // per 4 KiB piece; 0 = unpaced
   double budget_gbps = 0.0;      // shared by both directions; 0 = none
   int budget_priority = -1;      // direction that charges the budget without waiting
+  double share_gbps[2] = {0.0, 0.0};  // reserved part of the budget per direction
   int layer_group = 0;           // layered order: planes per group (0 = auto)
   unsigned long long* d_bucket = nullptr;
   int64_t launches = 0;
@@ -537,8 +620,8 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   p.stride = h->geo.plane_block_stride;
   p.host_block = h->geo.plane_chunk_bytes * h->geo.num_planes;
   p.num_planes = static_cast<uint32_t>(h->geo.num_planes);
-  // The bulk (TMA) path signals only whole-launch completion.
-  const bool bulk = h->path[dir] == KVS_PATH_BULK && !o.layered && o.op_flags == nullptr;
+  // Either path publishes every completion word (done / op / plane flags).
+  const bool bulk = h->path[dir] == KVS_PATH_BULK;
   int64_t piece = kPieceBytes;
   uint32_t stages = 0;
   if (bulk) {
@@ -584,6 +667,12 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   if (p.bucket_cost_ns == 0 && h->budget_gbps > 0.0) p.bucket_cost_ns = 1;
   p.bucket_burst_ns = 16 * p.bucket_cost_ns;
   p.bucket_nowait = h->budget_priority == dir ? 1u : 0u;
+  p.share = h->d_bucket + 1 + dir;
+  p.share_cost_ns = p.bucket_cost_ns != 0 && h->share_gbps[dir] > 0.0
+                        ? static_cast<uint64_t>(piece / h->share_gbps[dir] + 0.5)
+                        : 0;
+  if (p.share_cost_ns == 0 && p.bucket_cost_ns != 0 && h->share_gbps[dir] > 0.0)
+    p.share_cost_ns = 1;
   // Op / plane-group counters: zero at create; the warp that completes an op
   // (group) resets its counter, so the next launch of this direction (same
   // stream) starts from zero without a memset node.
@@ -601,7 +690,7 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   // The host ticket advances only once the launch is accepted: a failed
   // attribute call or launch must not leave it ahead of the device ticket
   // (every later done / end-of-plan flag of this direction would never fire).
-  const bool ticketed = o.done_flag != nullptr || (!bulk && o.layered && o.op_flags != nullptr);
+  const bool ticketed = o.done_flag != nullptr || (o.layered && o.op_flags != nullptr);
   if (bulk) {
     const size_t smem = static_cast<size_t>(stages) * static_cast<size_t>(piece);
     auto kern = dir == KVS_DIR_OUT ? kvs_swap_bulk_kernel<KVS_DIR_OUT, CAP>
@@ -707,8 +796,9 @@ int kvs_create(int device, const KvsGeometry* geo, const uint64_t* plane_ptrs, v
         cudaMemset(h->d_plane_ctr, 0, 2 * sizeof(unsigned long long) * geo->num_planes));
   if (!rc) rc = cuda_rc(cudaMalloc(&h->d_op_ctr, 2 * sizeof(uint32_t) * kOpsPerLaunchMax));
   if (!rc) rc = cuda_rc(cudaMemset(h->d_op_ctr, 0, 2 * sizeof(uint32_t) * kOpsPerLaunchMax));
-  if (!rc) rc = cuda_rc(cudaMalloc(&h->d_bucket, sizeof(unsigned long long)));
-  if (!rc) rc = cuda_rc(cudaMemset(h->d_bucket, 0, sizeof(unsigned long long)));
+  // [0] shared budget clock, [1 + dir] reserved-share clocks
+  if (!rc) rc = cuda_rc(cudaMalloc(&h->d_bucket, 3 * sizeof(unsigned long long)));
+  if (!rc) rc = cuda_rc(cudaMemset(h->d_bucket, 0, 3 * sizeof(unsigned long long)));
   if (rc) {
     kvs_destroy(h);
     return rc;
@@ -756,6 +846,14 @@ int kvs_set_budget_priority(KvsHandle* h, int dir) {
   if (h == nullptr || (dir != -1 && dir != KVS_DIR_OUT && dir != KVS_DIR_IN))
     return KVS_ERR_INVALID;
   h->budget_priority = dir;
+  return KVS_OK;
+}
+
+int kvs_set_budget_share(KvsHandle* h, int dir, double gbps) {
+  if (h == nullptr || (dir != KVS_DIR_OUT && dir != KVS_DIR_IN) || !(gbps >= 0.0) ||
+      gbps > 1e6)
+    return KVS_ERR_INVALID;
+  h->share_gbps[dir] = gbps;
   return KVS_OK;
 }
 

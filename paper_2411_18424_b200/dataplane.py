@@ -301,6 +301,11 @@ class SwapDataPlane:
         d = -1 if direction is None else _lib.DIRECTIONS[direction]
         _lib.check(self.lib.kvs_set_budget_priority(self.handle, d), "kvs_set_budget_priority")
 
+    def set_budget_share(self, direction: str, gbps: float = 0.0) -> None:
+        """Reserve `gbps` of the shared budget for `direction` (0 = none)."""
+        _lib.check(self.lib.kvs_set_budget_share(self.handle, _lib.DIRECTIONS[direction],
+                                                 float(gbps)), "kvs_set_budget_share")
+
     @property
     def launches(self) -> int:
         return int(self.lib.kvs_launch_count(self.handle))

@@ -105,6 +105,17 @@ class LiveStats:
     iterations: int = 0
     idle_waits: int = 0
     wall_s: float = 0.0
+    # per computing iteration: (decode kernel ms, KV bytes read, weight bytes
+    # streamed, swaps in flight, layered).  Layered iterations count their
+    # decode kernels only (per-layer events), not their plane-flag waits.
+    samples: list = None
+    solo_ms: tuple = (None, None)  # solo decode step before / after the run
+    bytes_per_us: float = 0.0  # calibrated solo decode rate (nominal times)
+    classified: str = "transfer pending at launch (host)"
+
+    def __post_init__(self) -> None:
+        if self.samples is None:
+            self.samples = []
 
     @property
     def decode_stall(self) -> float:
@@ -116,9 +127,83 @@ class LiveStats:
     def swap_induced_stall(self) -> Optional[float]:
         """Decode slowdown while swaps run, relative to decode with none in
         flight in the same run (same clocks, same power state)."""
-        if self.busy_nominal_ms <= 0 or self.quiet_nominal_ms <= 0 or self.quiet_ms <= 0:
+        if self.busy_nominal_ms <= 0 or self.quiet_ms <= 0 or self.quiet_nominal_ms <= 0:
             return None
         return (self.busy_ms / self.busy_nominal_ms) / (self.quiet_ms / self.quiet_nominal_ms) - 1
+
+    def classify_by_overlap(self, transfers: list) -> None:
+        """Re-label every decode sample by what actually ran beside it on the
+        device: busy if transfers overlapped >= half of its kernel interval,
+        quiet if none did; partial overlaps are dropped.  (The host-side flag
+        — "a transfer was pending at launch" — also marks decode that waited
+        for a transfer on the device and then ran alone.)  Recomputes the
+        busy / quiet sums behind swap_induced_stall."""
+        merged: list = []
+        for a, b in sorted(transfers):
+            if merged and a <= merged[-1][1]:
+                merged[-1][1] = max(merged[-1][1], b)
+            else:
+                merged.append([a, b])
+        starts = np.asarray([m[0] for m in merged])
+        out = []
+        self.busy_ms = self.busy_nominal_ms = self.quiet_ms = self.quiet_nominal_ms = 0.0
+        for smp in self.samples:
+            ms, kv, w, _, layered, t0, t1 = smp
+            i = int(np.searchsorted(starts, t1)) if merged else 0
+            ov = 0.0
+            for a, b in merged[max(0, i - 64):i]:
+                ov += max(0.0, min(b, t1) - max(a, t0))
+            frac = ov / (t1 - t0) if t1 > t0 else 0.0
+            if 0.0 < frac < 0.5:
+                continue
+            busy = frac >= 0.5
+            out.append((ms, kv, w, busy, layered, t0, t1))
+            nominal = (kv + w) / self.bytes_per_us / 1e3 if self.bytes_per_us else 0.0
+            if busy:
+                self.busy_ms += ms
+                self.busy_nominal_ms += nominal
+            else:
+                self.quiet_ms += ms
+                self.quiet_nominal_ms += nominal
+        self.samples = out
+        self.classified = "device overlap"
+
+    def stall_model(self, boot: int = 1000, seed: int = 0) -> Optional[dict]:
+        """Swap-induced decode stall controlled for the batch mix, with a 95%
+        bootstrap interval.
+
+        A quiet iteration's decode time is fitted as a + b*KV bytes + c*weight
+        bytes (least squares over every quiet iteration of the run: same
+        clocks, same power state, same kernels).  The stall is the busy
+        iterations' measured time over the fit's prediction for their own
+        mix, minus one.  The interval resamples quiet and busy iterations
+        (refitting each time), so a policy that costs nothing has an
+        interval around 0 — the noise floor the point estimate alone hides."""
+        if not self.samples:
+            return None
+        a = np.asarray([x[:4] for x in self.samples], dtype=np.float64)
+        busy = a[:, 3] > 0
+        q, b = a[~busy], a[busy]
+        if len(q) < 20 or len(b) < 5:
+            return None
+
+        def design(x):
+            return np.column_stack([np.ones(len(x)), x[:, 1] / 1e9, x[:, 2] / 1e9])
+
+        def stall(qx, bx):
+            coef, *_ = np.linalg.lstsq(design(qx), qx[:, 0], rcond=None)
+            pred = design(bx) @ coef
+            return float(bx[:, 0].sum() / max(1e-9, pred.sum()) - 1.0)
+
+        point = stall(q, b)
+        rng = np.random.default_rng(seed)
+        draws = [stall(q[rng.integers(0, len(q), len(q))], b[rng.integers(0, len(b), len(b))])
+                 for _ in range(boot)]
+        lo, hi = np.percentile(draws, [2.5, 97.5])
+        return {"stall": round(point, 4), "ci95": [round(float(lo), 4), round(float(hi), 4)],
+                "busy_iterations": int(len(b)), "quiet_iterations": int(len(q)),
+                "layered_iterations": int(sum(1 for x in self.samples if x[4])),
+                "busy_means": self.classified}
 
 
 class RankAgreement:
@@ -193,7 +278,7 @@ class LiveEngine(Engine):
         self._deferred: Optional[list] = None
         self.layered_joins = 0
         self.attend = attend and runtime.write_kv
-        self.live = LiveStats()
+        self.live = LiveStats(bytes_per_us=decode.bytes_per_us)
         # per computing iteration: (duration_us, cpu_us, wait_ms, kernel_ms,
         #                           synced, conflict_waits, n_prefill, n_decode)
         self._trace: list[tuple] = []
@@ -302,14 +387,29 @@ class LiveEngine(Engine):
         ex.compute.synchronize()
         torch.cuda.synchronize(dp.cache.device)
 
+    def solo_decode_ms(self, steps: int = 20, us: float = 2000.0) -> float:
+        """Median of `steps` solo decode steps of `us` modeled microseconds."""
+        comp = self.runtime.executor.compute
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        evs[0].record(comp)
+        for i in range(steps):
+            self.decode.launch_us(comp, us)
+            evs[i + 1].record(comp)
+        comp.synchronize()
+        return float(np.median([evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]))
+
     def run(self) -> MetricsReport:
         self.warmup()
+        before = self.solo_decode_ms()
         gc.collect()
         gc.freeze()  # long-lived engine state leaves the collector's young generations
         try:
-            return self._run()
+            rep = self._run()
         finally:
             gc.unfreeze()
+        self.runtime.synchronize()
+        self.live.solo_ms = (before, self.solo_decode_ms())
+        return rep
 
     def _run(self) -> MetricsReport:
         for conv in self.conversations:
@@ -327,6 +427,9 @@ class LiveEngine(Engine):
             self.agreement.clock(0)  # the TP group starts its clocks together
         self._landed = None
         self._t0 = time.perf_counter()
+        # Time origin on the device for this run's decode and transfer intervals.
+        self._ref_ev = torch.cuda.Event(enable_timing=True)
+        self._ref_ev.record(compute)
         self._skip = first_arrival
         wall0 = time.perf_counter()
 
@@ -430,14 +533,20 @@ class LiveEngine(Engine):
                 swapping = True
                 e0.record(compute)
                 planes = self.runtime.geometry.num_planes
-                nbytes = 0
+                kv_b = w_b = 0
+                layer_evs = []
                 for layer in range(planes):
                     for dep in layer_deps:
                         ex.wait_plane(compute, dep, layer)
+                    ea = torch.cuda.Event(enable_timing=True)
+                    ea.record(compute)  # this layer's KV has landed: decode starts
                     if reads:
-                        nbytes += self.runtime.attend(self, reads, planes=(layer, layer + 1))
+                        kv_b += self.runtime.attend(self, reads, planes=(layer, layer + 1))
                     if w_us > 0:
-                        nbytes += self.decode.launch_us(compute, w_us / planes)
+                        w_b += self.decode.launch_us(compute, w_us / planes)
+                    eb = torch.cuda.Event(enable_timing=True)
+                    eb.record(compute)
+                    layer_evs.append((ea, eb))
                 e1.record(compute)
                 self.runtime.write(self, spans)
             else:
@@ -446,9 +555,9 @@ class LiveEngine(Engine):
                 waits_seen = grant_waits + list(ex.last_barrier)
                 e0.record(compute)
                 swapping = any(not r.poll() for r in ex.pending)
-                nbytes = self.runtime.attend(self, reads) if reads else 0
-                if w_us > 0:
-                    nbytes += self.decode.launch_us(compute, w_us)
+                layer_evs = None
+                kv_b = self.runtime.attend(self, reads) if reads else 0
+                w_b = self.decode.launch_us(compute, w_us) if w_us > 0 else 0
                 e1.record(compute)
             compute.synchronize()
             if self._deferred:
@@ -461,16 +570,22 @@ class LiveEngine(Engine):
                                 kernel_ms, decision.mode == "sync" and bool(pending),
                                 conf_now, len(prefillers),
                                 len(decoders), waits_seen[:6], int((t_rt - t_cpu) * 1e6)))
-            nominal_ms = nbytes / self.decode.bytes_per_us / 1e3
-            if not layer_deps:  # layered steps include data waits: not a decode-rate sample
-                self.live.decode_ms += kernel_ms
-                self.live.decode_nominal_ms += nominal_ms
-                if swapping:
-                    self.live.busy_ms += kernel_ms
-                    self.live.busy_nominal_ms += nominal_ms
-                else:
-                    self.live.quiet_ms += kernel_ms
-                    self.live.quiet_nominal_ms += nominal_ms
+            nominal_ms = (kv_b + w_b) / self.decode.bytes_per_us / 1e3
+            # Layered steps include plane-flag waits: their decode sample is
+            # the per-layer kernel time, waits excluded.
+            dec_ms = kernel_ms if layer_evs is None else sum(a.elapsed_time(b)
+                                                            for a, b in layer_evs)
+            self.live.samples.append((dec_ms, kv_b, w_b, swapping, layer_evs is not None,
+                                      self._ref_ev.elapsed_time(e0),
+                                      self._ref_ev.elapsed_time(e1)))
+            self.live.decode_ms += dec_ms
+            self.live.decode_nominal_ms += nominal_ms
+            if swapping:
+                self.live.busy_ms += dec_ms
+                self.live.busy_nominal_ms += nominal_ms
+            else:
+                self.live.quiet_ms += dec_ms
+                self.live.quiet_nominal_ms += nominal_ms
             self.live.iterations += 1
             duration = end - start
             emitted = self._emit_tokens(prefillers, decoders, end)
@@ -501,6 +616,11 @@ class LiveEngine(Engine):
 
         self.runtime.synchronize()
         self.live.wall_s = time.perf_counter() - wall0
+        ex = self.runtime.executor
+        if ex.timing:
+            self.live.classify_by_overlap(
+                [(self._ref_ev.elapsed_time(r.start_event), self._ref_ev.elapsed_time(r.event))
+                 for r in ex.history if r.start_event is not None and r.nbytes])
         if self.attend:
             bad = self.runtime.kv_errors()
             if bad:
@@ -546,6 +666,10 @@ class LiveEngine(Engine):
                                           else round(self.live.swap_induced_stall, 4)),
             "decode_time_with_swaps_frac": round(
                 self.live.busy_ms / max(1e-9, self.live.decode_ms), 4),
+            "stall_model": self.live.stall_model(),
+            "solo_decode_ms": [None if x is None else round(x, 4) for x in self.live.solo_ms],
+            "solo_decode_drift": (None if None in self.live.solo_ms else
+                                  round(self.live.solo_ms[1] / self.live.solo_ms[0] - 1, 4)),
             "iterations": self.live.iterations,
             "idle_waits": self.live.idle_waits,
             "layered_joins": self.layered_joins,

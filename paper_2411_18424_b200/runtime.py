@@ -194,6 +194,56 @@ class Runtime:
                 "kv_bytes_read": self.kv_bytes_read,
                 "compute_waits": self.barrier_waits}
 
+    def swap_rates(self) -> dict:
+        """Swap GB/s while a transfer of each direction executes (needs
+        timing=True), and why it is what it is: transfers that ran alone vs
+        those that overlapped the other direction (host-link duplex), and
+        small vs large plans (fixed cost per launch)."""
+        recs = [r for r in self.executor.history if r.nbytes and r.start_event is not None]
+        if not recs:
+            return {}
+        self.synchronize()
+        ref = recs[0].start_event
+        iv = {"out": [], "in": []}
+        for r in recs:
+            iv[r.direction].append((ref.elapsed_time(r.start_event), ref.elapsed_time(r.event),
+                                    r.nbytes + r.refresh_bytes))
+
+        def merged(xs):
+            out = []
+            for a, b, _ in sorted(xs):
+                if out and a <= out[-1][1]:
+                    out[-1][1] = max(out[-1][1], b)
+                else:
+                    out.append([a, b])
+            return out
+
+        def rate(xs):
+            t = sum(b - a for a, b, _ in xs)
+            return round(sum(n for *_, n in xs) / (t * 1e-3) / 1e9, 2) if t > 0 else None
+
+        res = {}
+        for d, o in (("out", "in"), ("in", "out")):
+            xs, other = iv[d], merged(iv[o])
+            alone, duplex = [], []
+            for a, b, n in xs:
+                ov = sum(max(0.0, min(b, y) - max(a, x)) for x, y in other)
+                if b > a and ov / (b - a) < 0.1:
+                    alone.append((a, b, n))
+                elif b > a and ov / (b - a) > 0.9:
+                    duplex.append((a, b, n))
+            big = [x for x in xs if x[2] >= 32 << 20]
+            small = [x for x in xs if x[2] < 32 << 20]
+            res[d] = {"gib": round(sum(n for *_, n in xs) / 2**30, 2),
+                      "transfers": len(xs), "gbs_while_busy": rate(xs),
+                      "gbs_alone": rate(alone), "transfers_alone": len(alone),
+                      "gbs_overlapping_other_direction": rate(duplex),
+                      "transfers_overlapping": len(duplex),
+                      "gbs_plans_ge_32mib": rate(big), "gbs_plans_lt_32mib": rate(small),
+                      "mean_plan_mib": round(sum(n for *_, n in xs) / len(xs) / 2**20, 2)
+                      if xs else None}
+        return res
+
     def close(self) -> None:
         self.synchronize()
         self.dataplane.close()

@@ -205,13 +205,30 @@ COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 #                (both directions at once: 80 GB/s combined vs 75 with the
 #                LSU kernel, profiles/r01_duplex_mix.json; plan-level waits;
 #                decode pays for it);
+#   latency_share — latency, but swap-in holds a reserved 40 GB/s of the
+#                60 GB/s budget (kvs_set_budget_share): under FCFS a burst of
+#                preemptions leaves a concurrent resume ~10 GB/s; strict
+#                swap-in priority starves the preemptions instead;
+#   throughput_mix — bulk migration with one engine per direction: swap-out
+#                on the LSU kernel, swap-in on the copy engines (one batched
+#                copy per plan).  SM-issued host traffic in both directions
+#                tops out at 75-80 GB/s combined; LSU out + CE in measured
+#                87 GB/s (profiles/r01_duplex_mix.json); plan-level waits;
 #   unpaced    — out 8x512, in 32x512, no pacing (round-1 default shape).
 DUPLEX_POLICIES = {
     "latency": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0},
     # same, but swap-in draws on the shared budget first (kvs_set_budget_priority)
     "latency_in_first": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
                          "priority": "in"},
-    "throughput": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0, "path": "bulk"},
+    "latency_share": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
+                      "share": {"in": 40.0}},
+    # the serving policy on the TMA bulk kernels (op / plane flags from the
+    # elected thread's store side): same pace and budget, fewer SM threads
+    "latency_bulk": {"out": (8, 0, 52.0), "in": (8, 0, 0.0), "budget": 60.0, "path": "bulk"},
+    "throughput": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0, "path": "bulk",
+                   "signals": "plan"},
+    "throughput_mix": {"out": (16, 512, 0.0), "in": (8, 512, 0.0), "budget": 0.0,
+                       "engine": {"in": "ce_batch"}},
     "unpaced": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
 }
 
@@ -309,10 +326,16 @@ class StreamExecutor:
             self.dp.set_pace(direction, pace)
         self.dp.set_budget(pol["budget"])
         self.dp.set_budget_priority(pol.get("priority"))
-        # The TMA bulk kernel signals whole plans only: per-op / per-plane
-        # waits need the LSU kernel, so a bulk policy waits per plan.
-        self.op_granular = self._op_granular_wanted and path == "lsu"
-        self.layered_swap_in = self._layered_wanted and self.op_granular
+        for direction in ("out", "in"):
+            self.dp.set_budget_share(direction, pol.get("share", {}).get(direction, 0.0))
+        # Engine per direction: the kernel unless the policy routes one
+        # direction's plans to the copy engines (plan-level completion only).
+        self.engine = {d: pol.get("engine", {}).get(d, self.copy_impl) for d in ("out", "in")}
+        # Both kernel paths publish op / plane flags; a policy may choose
+        # plan-level completion only ("signals": "plan": bulk migration).
+        self.op_granular = self._op_granular_wanted and pol.get("signals", "op") == "op"
+        self.layered_swap_in = (self._layered_wanted and self.op_granular
+                                and self.engine["in"] == "kernel")
         self.duplex_policy = policy
 
     def _prune(self) -> None:
@@ -377,7 +400,7 @@ class StreamExecutor:
             start.record(stream)
         flag_base, seq, plane_base, span = None, 0, None, 0
         if ops:
-            if self.copy_impl == "kernel":
+            if self.engine[direction] == "kernel":
                 if self.op_granular:
                     layered = self.layered_swap_in and direction == "in"
                     span = len(ops) + (self.num_planes if layered else 0)
@@ -396,7 +419,7 @@ class StreamExecutor:
                     self.dp.swap(direction, ops, stream=stream)
                 self.launches += 1
             else:
-                mode = COPY_IMPLS.index(self.copy_impl) - 1
+                mode = COPY_IMPLS.index(self.engine[direction]) - 1
                 self.dp.baseline(direction, mode, ops, stream=stream)
         ev = torch.cuda.Event(enable_timing=self.timing)
         ev.record(stream)

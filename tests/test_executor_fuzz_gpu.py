@@ -35,7 +35,8 @@ SEEDS = int(os.environ.get("KVS_FUZZ_SEEDS", "1"))  # more for a soak run
 
 
 @pytest.mark.parametrize("seed", range(SEEDS))
-@pytest.mark.parametrize("mode", ["ops", "layered", "bulk", "partition"])
+@pytest.mark.parametrize("mode", ["ops", "layered", "bulk", "bulk_ops", "bulk_layered",
+                                  "partition"])
 def test_random_interleavings_match_program_order(cuda_ok, mode, seed):
     torch = cuda_ok
     from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
@@ -47,9 +48,13 @@ def test_random_interleavings_match_program_order(cuda_ok, mode, seed):
     cache = PagedKVCache(geo, G, device="cuda:0")
     host = HostKVPool(C, geo.block_bytes)
     dp = SwapDataPlane(cache, host)
-    ex = StreamExecutor(dp, duplex_policy="throughput" if mode == "bulk" else "latency",
-                        layered_swap_in=mode == "layered", sm_partition=8 if mode == "partition" else 0)
-    rng = np.random.default_rng([{"ops": 1, "layered": 2, "bulk": 3, "partition": 4}[mode], seed])
+    policy = {"bulk": "throughput", "bulk_ops": "latency_bulk",
+              "bulk_layered": "latency_bulk"}.get(mode, "latency")
+    ex = StreamExecutor(dp, duplex_policy=policy, layered_swap_in=mode.endswith("layered"),
+                        sm_partition=8 if mode == "partition" else 0)
+    assert ex.op_granular == (mode != "bulk")
+    rng = np.random.default_rng([{"ops": 1, "layered": 2, "bulk": 3, "partition": 4,
+                                  "bulk_ops": 5, "bulk_layered": 6}[mode], seed])
     last_in = None
     gpu = np.zeros((geo.num_planes, G, geo.plane_chunk_bytes), np.uint8)
     hostm = np.zeros((C, geo.block_bytes), np.uint8)
@@ -72,7 +77,7 @@ def test_random_interleavings_match_program_order(cuda_ok, mode, seed):
             ops = _extent_ops(rng, G, C)
             ex.submit("out", ops)
             orc.apply_plan("out", gpu, hostm, [(o.blocks, o.gpu_start, o.cpu_start) for o in ops])
-        elif a < 0.9 or last_in is None or mode != "layered":
+        elif a < 0.9 or last_in is None or not mode.endswith("layered"):
             ops = _extent_ops(rng, G, C)
             last_in = (ex.submit("in", ops), ops)
             orc.apply_plan("in", gpu, hostm, [(o.blocks, o.gpu_start, o.cpu_start) for o in ops])
