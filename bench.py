@@ -93,7 +93,7 @@ def parse(argv=None):
     ap.add_argument("--sm-partition", type=int, default=8,
                     help="serving + trace: swap kernels on their own N-SM green context, "
                          "decode on the rest (0 = share all SMs)")
-    ap.add_argument("--e2e-policy", default="throughput",
+    ap.add_argument("--e2e-policy", default="throughput_mix",
                     help="StreamExecutor duplex policy of the headline e2e leg")
     return ap.parse_args(argv)
 
@@ -491,6 +491,9 @@ def run_ours(args, geo):
 
     # ---- e2e: public API (control plane + dispatch) with host round trip ----
     e2e = run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, args.e2e_policy)
+    # the same leg with the kernel carrying both directions (TMA bulk), and
+    # under the serving policy (LSU, op flags, pace + budget)
+    e2e_kernel = run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, "throughput")
     e2e_serving = run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, "latency")
     dp.set_launch("out", args.ctas, 0)
     dp.set_launch("in", args.ctas, 0)
@@ -592,6 +595,7 @@ def run_ours(args, geo):
                                  "peak": measured_hbm_peak(), "unit": "GB/s"},
                          "ncu": ncu_link_rates()},
             "e2e": e2e,
+            "e2e_kernel_both_ways": e2e_kernel,
             "e2e_serving": e2e_serving,
             "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
@@ -616,10 +620,14 @@ def run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, policy):
 
     from paper_2411_18424_b200.costmodel import TransferParams
     from paper_2411_18424_b200.cpu_store import CpuStore
-    from paper_2411_18424_b200.swap import StreamExecutor, SwapManager
+    from paper_2411_18424_b200.swap import DUPLEX_POLICIES, StreamExecutor, SwapManager
     from paper_2411_18424_b200.synthetic import random_runs
 
     ex = StreamExecutor(dp, duplex_policy=policy)
+    path = DUPLEX_POLICIES[policy].get("path", "lsu")
+    engines = {d: (f"kernel ({'TMA bulk' if path == 'bulk' else 'LSU'})"
+                   if ex.engine[d] == "kernel" else f"copy engines ({ex.engine[d]})")
+               for d in ("out", "in")}
     mgr = SwapManager(TransferParams(), bytes_per_block=geo.block_bytes, executor=ex)
     gpu_pool, host_pool = pools(args.plan_blocks)
     store = CpuStore(host_pool, reuse_enabled=True)
@@ -683,10 +691,10 @@ def run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, policy):
     dp.set_budget_priority(None)
     return {"value": round(world * 2 * moved * args.steps / el / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": moved, "d2h_bytes_per_step": moved,
-            "policy": policy,
+            "policy": policy, "engines": engines,
             "api": f"CpuStore.plan_swap_out/plan_swap_in -> SwapManager.dispatch -> "
-                   f"StreamExecutor ({policy} policy) -> kvs_swap (C ABI); "
-                   f"wall clock incl. planning and sync",
+                   f"StreamExecutor ({policy} policy) -> kvs_swap / kvs_memcpy_baseline "
+                   f"(C ABI); wall clock incl. planning and sync",
             "requests_per_step": n_req, "gpu_launches": launches,
             "bytes_verified": verified}
 

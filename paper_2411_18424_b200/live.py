@@ -253,7 +253,8 @@ class LiveEngine(Engine):
 
     def __init__(self, config: EngineConfig, conversations, runtime, decode: DecodeEmulator,
                  time_scale: float = 1.0, agreement: Optional[RankAgreement] = None,
-                 layered: bool = False, attend: bool = True) -> None:
+                 layered: bool = False, attend: bool = True,
+                 per_layer_decode: bool = True) -> None:
         """layered: resumed requests join decode layer by layer (SURVEY §8f
         rank 2).  A swap-in at the head of the swap-in stream whose modeled
         completion falls inside this iteration joins the batch now, and so do
@@ -264,7 +265,13 @@ class LiveEngine(Engine):
         attend: each iteration also reads (and checks) the resident KV of
         every computing request, as attention would, inside the iteration's
         modeled time; any byte that differs from what its token wrote fails
-        the run (runtime.KVIntegrityError)."""
+        the run (runtime.KVIntegrityError).
+
+        per_layer_decode: a decode step is one attention + one weight-stream
+        kernel per layer (plane), as a model's layers are — in every
+        iteration, so a layered join's per-layer kernels and an ordinary
+        step's have the same launch structure and the swap-induced stall
+        compares like with like."""
         if runtime is None:
             raise ValueError("live mode needs a Runtime (real data plane)")
         super().__init__(config, conversations, runtime=runtime)
@@ -278,6 +285,7 @@ class LiveEngine(Engine):
         self._deferred: Optional[list] = None
         self.layered_joins = 0
         self.attend = attend and runtime.write_kv
+        self.per_layer_decode = per_layer_decode
         self.live = LiveStats(bytes_per_us=decode.bytes_per_us)
         # per computing iteration: (duration_us, cpu_us, wait_ms, kernel_ms,
         #                           synced, conflict_waits, n_prefill, n_decode)
@@ -535,13 +543,15 @@ class LiveEngine(Engine):
                 planes = self.runtime.geometry.num_planes
                 kv_b = w_b = 0
                 layer_evs = []
+                segs = self.runtime.read_segments(self, reads) if reads else None
                 for layer in range(planes):
                     for dep in layer_deps:
                         ex.wait_plane(compute, dep, layer)
                     ea = torch.cuda.Event(enable_timing=True)
                     ea.record(compute)  # this layer's KV has landed: decode starts
                     if reads:
-                        kv_b += self.runtime.attend(self, reads, planes=(layer, layer + 1))
+                        kv_b += self.runtime.attend(self, reads, planes=(layer, layer + 1),
+                                                   segs=segs)
                     if w_us > 0:
                         w_b += self.decode.launch_us(compute, w_us / planes)
                     eb = torch.cuda.Event(enable_timing=True)
@@ -556,8 +566,19 @@ class LiveEngine(Engine):
                 e0.record(compute)
                 swapping = any(not r.poll() for r in ex.pending)
                 layer_evs = None
-                kv_b = self.runtime.attend(self, reads) if reads else 0
-                w_b = self.decode.launch_us(compute, w_us) if w_us > 0 else 0
+                planes = self.runtime.geometry.num_planes
+                if self.per_layer_decode and planes > 1:
+                    kv_b = w_b = 0
+                    segs = self.runtime.read_segments(self, reads) if reads else None
+                    for layer in range(planes):
+                        if reads:
+                            kv_b += self.runtime.attend(self, reads, planes=(layer, layer + 1),
+                                                       segs=segs)
+                        if w_us > 0:
+                            w_b += self.decode.launch_us(compute, w_us / planes)
+                else:
+                    kv_b = self.runtime.attend(self, reads) if reads else 0
+                    w_b = self.decode.launch_us(compute, w_us) if w_us > 0 else 0
                 e1.record(compute)
             compute.synchronize()
             if self._deferred:

@@ -137,13 +137,20 @@ class Runtime:
         """KV bytes of one token across all planes (K and V)."""
         return self.geometry.block_bytes // self.geometry.block_tokens
 
-    def attend(self, engine, spans, planes: Optional[tuple[int, int]] = None) -> int:
+    def read_segments(self, engine, spans) -> np.ndarray:
+        """The resident-KV segments attend() reads for `spans` (reuse them
+        across the per-layer calls of one iteration)."""
+        return self.segments(engine, [(req, 0, lo) for req, lo, _ in spans])
+
+    def attend(self, engine, spans, planes: Optional[tuple[int, int]] = None,
+               segs: Optional[np.ndarray] = None) -> int:
         """Attention stand-in: read (and check) the resident KV of every
         computing request, tokens [0, lo) of each span, in `planes`; returns
         the bytes read.  Mismatches accumulate on the device (kv_errors())."""
         if not self.write_kv:
             return 0
-        segs = self.segments(engine, [(req, 0, lo) for req, lo, _ in spans])
+        if segs is None:
+            segs = self.read_segments(engine, spans)
         if not len(segs):
             return 0
         self.dataplane.kv_tokens(1, segs, stream=self.executor.compute,

@@ -205,15 +205,17 @@ COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 #                (both directions at once: 80 GB/s combined vs 75 with the
 #                LSU kernel, profiles/r01_duplex_mix.json; plan-level waits;
 #                decode pays for it);
-#   latency_share — latency, but swap-in holds a reserved 40 GB/s of the
+#   latency_share — latency, but swap-in holds a reserved 42 GB/s of the
 #                60 GB/s budget (kvs_set_budget_share): under FCFS a burst of
 #                preemptions leaves a concurrent resume ~10 GB/s; strict
 #                swap-in priority starves the preemptions instead;
 #   throughput_mix — bulk migration with one engine per direction: swap-out
-#                on the LSU kernel, swap-in on the copy engines (one batched
-#                copy per plan).  SM-issued host traffic in both directions
-#                tops out at 75-80 GB/s combined; LSU out + CE in measured
-#                87 GB/s (profiles/r01_duplex_mix.json); plan-level waits;
+#                on the TMA bulk kernel, swap-in on the copy engines (one
+#                batched copy per plan).  SM-issued host traffic in both
+#                directions tops out at 75-80 GB/s combined; the e2e leg
+#                measured bulk out + CE in at 88.3 GB/s vs 78.4 bulk both ways
+#                and 84.8 LSU out + CE in (profiles/r02_e2e_policy_probe.json);
+#                plan-level waits;
 #   unpaced    — out 8x512, in 32x512, no pacing (round-1 default shape).
 DUPLEX_POLICIES = {
     "latency": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0},
@@ -221,14 +223,14 @@ DUPLEX_POLICIES = {
     "latency_in_first": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
                          "priority": "in"},
     "latency_share": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
-                      "share": {"in": 40.0}},
+                      "share": {"in": 42.0}},
     # the serving policy on the TMA bulk kernels (op / plane flags from the
     # elected thread's store side): same pace and budget, fewer SM threads
     "latency_bulk": {"out": (8, 0, 52.0), "in": (8, 0, 0.0), "budget": 60.0, "path": "bulk"},
     "throughput": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0, "path": "bulk",
                    "signals": "plan"},
-    "throughput_mix": {"out": (16, 512, 0.0), "in": (8, 512, 0.0), "budget": 0.0,
-                       "engine": {"in": "ce_batch"}},
+    "throughput_mix": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0,
+                       "path": "bulk", "engine": {"in": "ce_batch"}, "signals": "plan"},
     "unpaced": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
 }
 

@@ -55,7 +55,9 @@ def run_one(args, mode, impl, decode, geo):
             nbytes[r.direction] += r.nbytes + r.refresh_bytes
     out = {
         "mode": mode, "copy_impl": impl, "wall_s": round(wall, 2),
+        "policy": args.policy, "layered": args.layered, "sm_partition": args.sm_partition,
         "latency": lat,
+        "swap_rates": rt.swap_rates(),
         "report": {k: v for k, v in rep.to_dict().items() if k != "granularity_histogram"},
         "swap": {d: {"bytes": nbytes[d], "gbs_while_busy": round(nbytes[d] / secs[d] / 1e9, 2)
                      if secs[d] else None, "transfers": sum(1 for r in ex.history
@@ -108,8 +110,10 @@ def main():
         mode, impl = item.split(":")
         res = run_one(args, mode, impl, decode, geo)
         results["runs"].append(res)
-        print(json.dumps({k: res[k] for k in ("mode", "copy_impl", "wall_s", "latency", "swap",
-                                              "slowest_transfers_ms", "ttft_anatomy")}),
+        print(json.dumps({k: res[k] for k in ("mode", "copy_impl", "policy", "layered",
+                                              "sm_partition", "wall_s", "latency", "swap",
+                                              "swap_rates", "slowest_transfers_ms",
+                                              "ttft_anatomy")}),
               flush=True)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
