@@ -95,6 +95,8 @@ def parse(argv=None):
                          "decode on the rest (0 = share all SMs)")
     ap.add_argument("--e2e-policy", default="throughput_mix",
                     help="StreamExecutor duplex policy of the headline e2e leg")
+    ap.add_argument("--serving-policy", default="serving",
+                    help="StreamExecutor duplex policy of the live traces' FastSwitch arm")
     return ap.parse_args(argv)
 
 
@@ -524,13 +526,15 @@ def run_ours(args, geo):
     # ---- serving configuration: paced swaps under a concurrent decode load ----
     serving = None
     if rank == 0:
-        pol = os.environ.get("KVS_SERVING_POLICY", "latency")
-        serving = {"shared_sms": serving_interference(dp, dev, s, 0, pol)}
+        serving = {"full_rate_shared_sms": serving_interference(dp, dev, s, 0, "latency")}
         if args.sm_partition:
             part = f"swap_on_{args.sm_partition}_sms"
-            serving[part] = serving_interference(dp, dev, s, args.sm_partition, pol)
-            serving[part + "_in_share"] = serving_interference(dp, dev, s, args.sm_partition,
+            serving["full_rate_" + part] = serving_interference(dp, dev, s, args.sm_partition,
+                                                                "latency")
+            serving["in_share_" + part] = serving_interference(dp, dev, s, args.sm_partition,
                                                                "latency_share")
+            serving[args.serving_policy + "_" + part] = serving_interference(
+                dp, dev, s, args.sm_partition, args.serving_policy)
 
     # ---- live multi-turn preemption traces: P99 TTFT / TBT (metric part 2) ----
     trace = None
@@ -735,8 +739,10 @@ def run_trace(args, geo, dev, name):
     out = {"workload": f"{t['convs']} conversations, {t['rate']:g} req/s, think "
                        f"{t['think']:g} s, 512 x {geo.block_bytes / 2**20:g} MiB GPU blocks "
                        f"per rank (TP{world}), {t['cpu']}-block host pool, {t['pattern']} "
-                       f"priorities f=0.04, decode = {decode.bytes_per_us / 1e3:.0f} GB/s "
-                       f"weight streaming per rank + KV reads of every resident token",
+                       f"priorities f=0.04, decode = {geo.num_planes} per-layer steps of "
+                       f"KV reads of every resident token + {decode.bytes_per_us / 1e3:.0f} GB/s "
+                       f"weight streaming per rank; FastSwitch swaps under the "
+                       f"'{args.serving_policy}' policy",
            "pattern": t["pattern"], "tp": world, "sm_partition": sms, "runs": {}}
     for run, mode, impl in (("fastswitch", "full", "kernel"),
                             ("vllm_like", "baseline", "ce_per_block")):
@@ -745,7 +751,8 @@ def run_trace(args, geo, dev, name):
         layered = impl == "kernel" and not args.no_layered
         rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, device=dev,
                      copy_impl=impl, timing=True, sm_partition=args.sm_partition,
-                     layered_swap_in=layered)
+                     layered_swap_in=layered,
+                     duplex_policy=args.serving_policy if impl == "kernel" else "latency")
         eng = LiveEngine(cfg, generate(wl), rt, decode, agreement=agreement, layered=layered)
         eng.turn_trace = []
         rep = eng.run()
@@ -774,8 +781,10 @@ def run_trace(args, geo, dev, name):
     return out
 
 
-def serving_interference(dp, dev, s, sm_partition: int = 0, policy: str = "latency"):
-    """Swap-induced decode stall, measured: 2 ms HBM-streaming decode steps on a
+def serving_interference(dp, dev, s, sm_partition: int = 0, policy: str = "latency",
+                         layers: int = 32):
+    """Swap-induced decode stall, measured: 2 ms HBM-streaming decode steps
+    (each `layers` per-layer kernels, as the live engine runs them) on a
     high-priority stream while a 2 GiB swap runs, per direction and both at
     once, under a serving policy (swap.DUPLEX_POLICIES: paced kernels, shared
     budget, optional reserved share)."""
@@ -807,7 +816,8 @@ def serving_interference(dp, dev, s, sm_partition: int = 0, policy: str = "laten
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
         evs[0].record(comp)
         for i in range(k):
-            dec.launch_us(comp, 2000.0)
+            for _ in range(layers):
+                dec.launch_us(comp, 2000.0 / layers)
             evs[i + 1].record(comp)
         return evs
 
@@ -826,7 +836,7 @@ def serving_interference(dp, dev, s, sm_partition: int = 0, policy: str = "laten
     dp.set_budget(pol["budget"])
     dp.set_budget_priority(pol.get("priority"))
     out = {"policy": policy, "sm_partition": sms, "decode_step_solo_ms": round(solo, 3),
-           "runs": {}}
+           "decode_kernels_per_step": layers, "runs": {}}
     for name, dirs in (("out", ("out",)), ("in", ("in",)), ("duplex", ("out", "in"))):
         torch.cuda.synchronize()
         t = {}

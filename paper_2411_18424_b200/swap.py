@@ -224,6 +224,12 @@ DUPLEX_POLICIES = {
                          "priority": "in"},
     "latency_share": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
                       "share": {"in": 42.0}},
+    # serving: paced below the link in both directions.  A decode step made
+    # of per-layer kernels pays ~0.2-0.4% per GB/s of concurrent swap-in HBM
+    # writes (profiles/r02_interference_layers.json); on the live trace swap-in
+    # 40 / swap-out 20 GB/s holds the stall under 10% with the same TTFT tail
+    # as full rate (profiles/r02_live_policy_probe.json).
+    "serving": {"out": (8, 512, 20.0), "in": (8, 256, 40.0), "budget": 60.0},
     # the serving policy on the TMA bulk kernels (op / plane flags from the
     # elected thread's store side): same pace and budget, fewer SM threads
     "latency_bulk": {"out": (8, 0, 52.0), "in": (8, 0, 0.0), "budget": 60.0, "path": "bulk"},

@@ -51,3 +51,7 @@ def test_duplex_policies_are_well_formed():
     lat = DUPLEX_POLICIES["latency"]
     assert 0 < lat["out"][2] < 63.0
     assert lat["in"][2] == 0.0 and lat["in"][0] * lat["in"][1] // 32 * 4096 <= 512 * 1024
+    # the live traces' policy: both directions paced below the link, under the budget
+    srv = DUPLEX_POLICIES["serving"]
+    assert 0 < srv["out"][2] <= srv["in"][2] < 63.0
+    assert srv["out"][2] + srv["in"][2] <= srv["budget"]

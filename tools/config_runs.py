@@ -35,6 +35,7 @@ from paper_2411_18424_b200.workload import generate  # noqa: E402
 
 SM_PARTITION = int(os.environ.get("SM_PARTITION", "8"))
 LAYERED = os.environ.get("LAYERED", "1") == "1"  # FastSwitch runs with layered admission
+POLICY = os.environ.get("POLICY", "serving")  # FastSwitch's swap policy (swap.DUPLEX_POLICIES)
 
 
 def swap_rates(rt):
@@ -54,7 +55,8 @@ def live_run(geo, doc, impl="kernel", decode=None, verify=False):
     cfg = dataclasses.replace(cfg, transfer=b200_transfer_params())
     layered = LAYERED and impl == "kernel"
     rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, copy_impl=impl,
-                 verify=verify, timing=True, sm_partition=SM_PARTITION, layered_swap_in=layered)
+                 verify=verify, timing=True, sm_partition=SM_PARTITION, layered_swap_in=layered,
+                 duplex_policy=POLICY if impl == "kernel" else "latency")
     eng = LiveEngine(cfg, generate(wl), rt, decode, layered=layered)
     eng.turn_trace = []
     t0 = time.perf_counter()

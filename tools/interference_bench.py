@@ -27,13 +27,17 @@ from paper_2411_18424_b200.live import DecodeEmulator  # noqa: E402
 
 STEP_US = 2000.0
 POOL = 4096
+# DECODE_LAYERS=L: a step is L weight-stream kernels of STEP_US / L each (a
+# model's per-layer kernels) instead of one STEP_US kernel.
+LAYERS = int(os.environ.get("DECODE_LAYERS", "1"))
 
 
 def decode_steps(dec, stream, n):
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(n + 1)]
     evs[0].record(stream)
     for i in range(n):
-        dec.launch_us(stream, STEP_US)
+        for _ in range(LAYERS):
+            dec.launch_us(stream, STEP_US / LAYERS)
         evs[i + 1].record(stream)
     return evs
 
@@ -69,6 +73,7 @@ def main():
     torch.cuda.synchronize()
     solo = statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(40))
     results = {"decode_step_solo_ms": round(solo, 4), "decode_ctas": dec.ctas,
+               "decode_layers": LAYERS,
                "sm_partition": sms, "runs": []}
     print(json.dumps(results), flush=True)
 
@@ -121,6 +126,31 @@ def main():
                         {"out": 52.0, "in": 0.0}, "kernel", ("out",)))
         configs.append(("duplex", "lsu", {"out": (8, 512), "in": (8, 256)},
                         {"out": 52.0, "in": 0.0}, "kernel", ("out", "in")))
+    elif sweep == "layers":
+        # the serving policy's shapes, and swap-in paced lower
+        for pace in (0.0, 40.0, 30.0, 20.0):
+            configs.append((f"in8x256p{pace:g}", "lsu", {"out": (8, 512), "in": (8, 256)},
+                            {"out": 0.0, "in": pace}, "kernel", ("in",)))
+        configs.append(("out8x512p52", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 52.0, "in": 0.0}, "kernel", ("out",)))
+        configs.append(("out8x512p30", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 30.0, "in": 0.0}, "kernel", ("out",)))
+        configs.append(("bulk_in8", "bulk", {"out": (8, 32), "in": (8, 32)},
+                        {"out": 0.0, "in": 0.0}, "kernel", ("in",)))
+        configs.append(("ce_batch_in", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 0.0, "in": 0.0}, "ce_batch", ("in",)))
+        configs.append(("ce_batch_out", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 0.0, "in": 0.0}, "ce_batch", ("out",)))
+    elif sweep == "floor":
+        # is there a cost of a running swap kernel that does not scale with its rate?
+        for pace in (2.0, 5.0, 10.0, 20.0):
+            configs.append((f"in8x256p{pace:g}", "lsu", {"out": (8, 512), "in": (8, 256)},
+                            {"out": 0.0, "in": pace}, "kernel", ("in",)))
+            configs.append((f"in1x32p{pace:g}", "lsu", {"out": (8, 512), "in": (1, 32)},
+                            {"out": 0.0, "in": pace}, "kernel", ("in",)))
+        for pace in (5.0, 20.0):
+            configs.append((f"out8x512p{pace:g}", "lsu", {"out": (8, 512), "in": (8, 256)},
+                            {"out": pace, "in": 0.0}, "kernel", ("out",)))
     elif sweep == "in":
         for ct in ((16, 512), (32, 128), (64, 64), (148, 32)):
             for pace in (0.0, 48.0, 40.0):

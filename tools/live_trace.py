@@ -38,7 +38,8 @@ def run_one(args, mode, impl, decode, geo):
     rt = Runtime(geo, cfg.gpu_pool.total_blocks, cfg.cpu_pool_blocks, copy_impl=impl,
                  verify=args.verify, timing=True, duplex_policy=args.policy,
                  sm_partition=args.sm_partition, layered_swap_in=args.layered)
-    eng = LiveEngine(cfg, generate(wl), rt, decode, layered=args.layered and impl == "kernel")
+    eng = LiveEngine(cfg, generate(wl), rt, decode, layered=args.layered and impl == "kernel",
+                     per_layer_decode=not args.single_kernel_decode)
     eng.turn_trace = []
     t0 = time.perf_counter()
     rep = eng.run()
@@ -95,6 +96,11 @@ def main():
                     help="swap kernels on their own N-SM green context, decode on the rest")
     ap.add_argument("--layered", action="store_true",
                     help="resumed requests join decode layer by layer (plane flags)")
+    ap.add_argument("--decode-ctas", type=int, default=0,
+                    help="decode weight-stream kernel: 0 = 2 persistent CTAs per compute SM, "
+                         "<0 = one CTA per -N KiB tile (block-scheduler balanced)")
+    ap.add_argument("--single-kernel-decode", action="store_true",
+                    help="one weight-stream kernel per step instead of one per layer")
     ap.add_argument("--out", default="gpurun_out/live_trace.json")
     args = ap.parse_args()
     geo = PRESETS[args.model]
@@ -103,6 +109,8 @@ def main():
         from paper_2411_18424_b200.swap import partition_streams
         _, stream, sms = partition_streams(torch.device("cuda:0"), args.sm_partition)
         ctas = 2 * sms[1]
+    if args.decode_ctas:
+        ctas = args.decode_ctas
     decode = DecodeEmulator("cuda:0", weight_bytes=args.weights_gib << 30, ctas=ctas,
                             stream=stream)
     results = {"decode_calibrated_gbs": round(decode.bytes_per_us / 1e3, 1), "runs": []}
@@ -110,7 +118,9 @@ def main():
         mode, impl = item.split(":")
         res = run_one(args, mode, impl, decode, geo)
         results["runs"].append(res)
-        print(json.dumps({k: res[k] for k in ("mode", "copy_impl", "policy", "layered",
+        res["decode"] = {"ctas": ctas, "per_layer": not args.single_kernel_decode,
+                         "calibrated_gbs": results["decode_calibrated_gbs"]}
+        print(json.dumps({k: res[k] for k in ("mode", "copy_impl", "policy", "layered", "decode",
                                               "sm_partition", "wall_s", "latency", "swap",
                                               "swap_rates", "slowest_transfers_ms",
                                               "ttft_anatomy")}),
