@@ -7,6 +7,8 @@ oracle; BASELINE-size shapes use the round-trip property
 (out -> poison HBM -> in to a different table == original).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -673,11 +675,12 @@ def test_budget_share_reserves_a_rate_for_one_direction(cuda_ok):
     torch.cuda.synchronize()
     in_gbs = 128 * LLAMA3_8B.block_bytes / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9
     out_ms = ev[0].elapsed_time(ev[1])
-    assert in_gbs >= 0.85 * 15.0, in_gbs
-    # the budget still binds the pair: out + in together stay near 20 GB/s
-    total = (256 + 128) * LLAMA3_8B.block_bytes / (max(out_ms, ev[0].elapsed_time(ev[3]))
-                                                    * 1e-3) / 1e9
-    assert total <= 1.15 * 20.0, total
+    if "CUDA_INJECTION64_PATH" not in os.environ:  # rates mean nothing under compute-sanitizer
+        assert in_gbs >= 0.85 * 15.0, in_gbs
+        # the budget still binds the pair: out + in together stay near 20 GB/s
+        total = (256 + 128) * LLAMA3_8B.block_bytes / (
+            max(out_ms, ev[0].elapsed_time(ev[3])) * 1e-3) / 1e9
+        assert total <= 1.15 * 20.0, total
     got = host.tensor[0:256].cuda().view(256, LLAMA3_8B.num_planes, -1).permute(1, 0, 2)
     assert torch.equal(got, src)
     assert (cache.planes[:, 512:640].cpu().numpy() == 0x3C).all()
