@@ -396,7 +396,8 @@ def workload_config(args, geo) -> dict:
             "plan_blocks": args.plan_blocks, "group_blocks": args.group,
             "gpu_pool_blocks": pools(args.plan_blocks)[0],
             "host_pool_blocks": pools(args.plan_blocks)[1],
-            "l2": f"inputs {nb / 2**30:g} GiB/direction > 126 MB L2, no flush"}
+            "l2": f"inputs {nb / 2**30:g} GiB/direction > 126 MB L2, no flush",
+            "parallelism": f"replicas{args.gpus} (per-rank KV shard, own PCIe link)"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -563,11 +564,7 @@ def run_ours(args, geo):
         dominant, dom_ms = ("in", in_ms) if sum(in_ms) >= sum(out_ms) else ("out", out_ms)
         achieved = nbytes_dir / (statistics.mean(dom_ms) * 1e-3) / 1e9
         traffic = ncu_traffic(dominant)
-        config = workload_config(args, geo)
-        config.update({
-            "parallelism": f"replicas{world} (per-rank KV shard, own PCIe link)",
-            "host_pool": {"blocks": host_pool, "numa_node": host_numa,
-                          "numa_node_per_rank": numa_per_rank, "numa_nodes": numa_nodes()}})
+        config = workload_config(args, geo)  # identical to the reference arm's
         ce_sum = {d: round(sum(c[d] for c in ce_all), 3) for d in ("out", "in")}
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
@@ -577,6 +574,8 @@ def run_ours(args, geo):
             "data": "synthetic (random KV bytes, seeded random block tables)",
             "backend": backend if world > 1 else None,
             "config": config,
+            "host_pool": {"blocks": host_pool, "numa_node": host_numa,
+                          "numa_node_per_rank": numa_per_rank, "numa_nodes": numa_nodes()},
             "per_direction_gbs": {"out": round(out_gbs, 3), "in": round(in_gbs, 3)},
             "roofline": {"bound": "pcie", "achieved": round(achieved, 3),
                          "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
