@@ -141,9 +141,17 @@ def main():
                         {"out": 0.0, "in": 0.0}, "ce_batch", ("in",)))
         configs.append(("ce_batch_out", "lsu", {"out": (8, 512), "in": (8, 256)},
                         {"out": 0.0, "in": 0.0}, "ce_batch", ("out",)))
+    elif sweep == "knee":
+        # swap-in pace just below the link rate: where does the cost jump?
+        for pace in (30.0, 36.0, 40.0, 44.0, 46.0, 48.0, 50.0, 0.0):
+            configs.append((f"in8x256p{pace:g}", "lsu", {"out": (8, 512), "in": (8, 256)},
+                            {"out": 0.0, "in": pace}, "kernel", ("in",)))
+        for pace in (20.0, 30.0, 40.0, 48.0, 52.0):
+            configs.append((f"out8x512p{pace:g}", "lsu", {"out": (8, 512), "in": (8, 256)},
+                            {"out": pace, "in": 0.0}, "kernel", ("out",)))
     elif sweep == "floor":
         # is there a cost of a running swap kernel that does not scale with its rate?
-        for pace in (2.0, 5.0, 10.0, 20.0):
+        for pace in (0.01, 0.1, 2.0, 5.0, 10.0, 20.0):
             configs.append((f"in8x256p{pace:g}", "lsu", {"out": (8, 512), "in": (8, 256)},
                             {"out": 0.0, "in": pace}, "kernel", ("in",)))
             configs.append((f"in1x32p{pace:g}", "lsu", {"out": (8, 512), "in": (1, 32)},
@@ -176,9 +184,18 @@ def main():
             dp.set_pace(d, pace[d])
         torch.cuda.synchronize()
         t = {}
+        moved = {}
         for d in dirs:
             st = s_out if d == "out" else s_in
             ops = ops_out if d == "out" else ops_in
+            if 0.0 < pace[d] < 10.0:
+                # slow paces: only ~0.5 s worth of bytes (decode is sampled for ~0.2 s)
+                keep = max(1, int(pace[d] * 1e9 * 0.5 / geo.block_bytes))
+                ops = orc.random_runs(np.random.default_rng(1), keep, 1, half, half).astype(
+                    np.int32)
+                if d == "in":
+                    ops[:, 1:] += half
+            moved[d] = int(np.asarray(ops)[:, 0].sum()) * geo.block_bytes
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             if impl == "kernel":
@@ -200,7 +217,7 @@ def main():
                "dirs": "+".join(dirs), "decode_steps_overlapped": len(steps),
                "decode_slowdown": round(statistics.median(steps) / solo - 1, 4) if steps else None,
                "decode_slowdown_mean": round(statistics.mean(steps) / solo - 1, 4) if steps else None,
-               "swap_gbs": {d: round(nbytes / (t[d][0].elapsed_time(t[d][1]) * 1e-3) / 1e9, 2)
+               "swap_gbs": {d: round(moved[d] / (t[d][0].elapsed_time(t[d][1]) * 1e-3) / 1e9, 2)
                             for d in dirs}}
         results["runs"].append(row)
         print(json.dumps(row), flush=True)
