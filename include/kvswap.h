@@ -116,6 +116,12 @@ int kvs_set_path(KvsHandle* h, int dir, int path, int piece_bytes, int stages);
  * Replaces the reference's bounded dispatch yield (swap.py:256-268). */
 int kvs_set_pace(KvsHandle* h, int dir, double gbps);
 
+/* Release a paced direction's pieces in bursts of `burst_bytes` (0 = steady)
+ * at the same mean rate: the grid moves a burst at full speed, then idles
+ * until the pace catches up.  Probes whether HBM writes batched in time cost
+ * decode less than the same bytes spread evenly. */
+int kvs_set_pace_burst(KvsHandle* h, int dir, int64_t burst_bytes);
+
 /* One rate budget shared by both directions of this handle (0 = none): a
  * token bucket on the GPU global timer, drawn per piece by swap-out and
  * swap-in kernels alike, so a concurrent preempt + resume cannot add up to

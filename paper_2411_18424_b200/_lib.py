@@ -50,6 +50,7 @@ EXPORTED_SYMBOLS = (
     "kvs_set_budget",
     "kvs_set_budget_priority",
     "kvs_set_budget_share",
+    "kvs_set_pace_burst",
     "kvs_swap",
     "kvs_swap_layered",
     "kvs_set_layer_group",
@@ -121,6 +122,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_set_budget.argtypes = [c.c_void_p, c.c_double]
     lib.kvs_set_budget_priority.restype = c.c_int
     lib.kvs_set_budget_priority.argtypes = [c.c_void_p, c.c_int]
+    lib.kvs_set_pace_burst.restype = c.c_int
+    lib.kvs_set_pace_burst.argtypes = [c.c_void_p, c.c_int, c.c_int64]
     lib.kvs_set_budget_share.restype = c.c_int
     lib.kvs_set_budget_share.argtypes = [c.c_void_p, c.c_int, c.c_double]
     lib.kvs_set_layer_group.restype = c.c_int

@@ -69,6 +69,7 @@ struct SwapParams {
   uint32_t* op_ctr;            // [n_ops] piece counters, zeroed before the launch
   uint32_t* op_flags;          // [n_ops]: receives seq when a TransferOp has landed
   uint64_t pace_ps;            // >0: piece i may start no earlier than t0 + i*pace_ps
+  uint32_t pace_burst;         // >0: pieces released in bursts of this many (same mean rate)
   unsigned long long* bucket;  // shared (both directions) budget clock, ns
   uint64_t bucket_cost_ns;     // >0: ns of budget one piece consumes
   uint64_t bucket_burst_ns;    // idle credit cap
@@ -257,8 +258,10 @@ __global__ void __launch_bounds__(kMaxThreads)
     if (p.pace_ps != 0) {
       // Rate pacing: posted sysmem stores (and, less so, non-posted reads)
       // issued faster than PCIe drains them back up the XBAR/L2 queues the
-      // decode kernel's HBM traffic shares.  Hold the grid to the link rate.
-      const uint64_t due = t0 + (static_cast<uint64_t>(i) * p.pace_ps) / 1000u;
+      // decode kernel's HBM traffic shares.  Hold the grid to the link rate
+      // (optionally releasing pieces in bursts at the same mean rate).
+      const uint64_t ii = p.pace_burst ? (i / p.pace_burst) * p.pace_burst : i;
+      const uint64_t due = t0 + (ii * p.pace_ps) / 1000u;
       while (globaltimer_ns() < due) __nanosleep(64);
     }
     if (p.bucket_cost_ns != 0) {
@@ -466,7 +469,8 @@ __global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant
     // Pacing (kvs_set_pace): piece i's load may not issue before t0 + i*pace.
     auto pace = [&](uint32_t i) {
       if (p.pace_ps != 0) {
-        const uint64_t due = t0 + (static_cast<uint64_t>(i) * p.pace_ps) / 1000u;
+        const uint64_t ii = p.pace_burst ? (i / p.pace_burst) * p.pace_burst : i;
+        const uint64_t due = t0 + (ii * p.pace_ps) / 1000u;
         while (globaltimer_ns() < due) __nanosleep(64);
       }
       if (p.bucket_cost_ns != 0) {
@@ -563,6 +567,7 @@ struct KvsHandle {
   int piece_bytes[2] = {0, 0};
   int stages[2] = {0, 0};
   uint64_t pace_ps[2] = {0, 0};  // per 4 KiB piece; 0 = unpaced
+  int64_t pace_burst_bytes[2] = {0, 0};  // 0 = steady pacing
   double budget_gbps = 0.0;      // shared by both directions; 0 = none
   int budget_priority = -1;      // direction that charges the budget without waiting
   double share_gbps[2] = {0.0, 0.0};  // reserved part of the budget per direction
@@ -661,6 +666,9 @@ int launch_cap(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, int64_t
   p.op_flags = o.op_flags;
   // pace_ps is per 4 KiB; the bulk path paces per (larger) TMA piece.
   p.pace_ps = h->pace_ps[dir] * static_cast<uint64_t>(piece) / kPieceBytes;
+  p.pace_burst = h->pace_burst_bytes[dir] > piece
+                     ? static_cast<uint32_t>(h->pace_burst_bytes[dir] / piece)
+                     : 0u;
   p.bucket = h->d_bucket;
   p.bucket_cost_ns =
       h->budget_gbps > 0.0 ? static_cast<uint64_t>(piece / h->budget_gbps + 0.5) : 0;
@@ -833,6 +841,13 @@ int kvs_set_pace(KvsHandle* h, int dir, double gbps) {
     return KVS_ERR_INVALID;
   // ps per 4 KiB piece at `gbps` GB/s (1 GB/s = 1 byte/ns).
   h->pace_ps[dir] = gbps == 0.0 ? 0 : static_cast<uint64_t>(kPieceBytes * 1000.0 / gbps + 0.5);
+  return KVS_OK;
+}
+
+int kvs_set_pace_burst(KvsHandle* h, int dir, int64_t burst_bytes) {
+  if (h == nullptr || (dir != KVS_DIR_OUT && dir != KVS_DIR_IN) || burst_bytes < 0)
+    return KVS_ERR_INVALID;
+  h->pace_burst_bytes[dir] = burst_bytes;
   return KVS_OK;
 }
 

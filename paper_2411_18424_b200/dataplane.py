@@ -288,6 +288,11 @@ class SwapDataPlane:
         _lib.check(self.lib.kvs_set_pace(self.handle, _lib.DIRECTIONS[direction], float(gbps)),
                    "kvs_set_pace")
 
+    def set_pace_burst(self, direction: str, burst_bytes: int = 0) -> None:
+        """Release paced pieces in bursts of `burst_bytes` (0 = steady)."""
+        _lib.check(self.lib.kvs_set_pace_burst(self.handle, _lib.DIRECTIONS[direction],
+                                               int(burst_bytes)), "kvs_set_pace_burst")
+
     def set_budget(self, gbps: float = 0.0) -> None:
         """One GB/s budget shared by swap-out and swap-in (0 = none)."""
         _lib.check(self.lib.kvs_set_budget(self.handle, float(gbps)), "kvs_set_budget")

@@ -141,6 +141,13 @@ def main():
                         {"out": 0.0, "in": 0.0}, "ce_batch", ("in",)))
         configs.append(("ce_batch_out", "lsu", {"out": (8, 512), "in": (8, 256)},
                         {"out": 0.0, "in": 0.0}, "ce_batch", ("out",)))
+    elif sweep == "burst":
+        # same mean swap-in rate, released steadily or in bursts (kvs_set_pace_burst)
+        for pace in (10.0, 20.0, 40.0):
+            for burst in (0, 1 << 20, 8 << 20, 32 << 20):
+                configs.append((f"in8x256p{pace:g}b{burst >> 20}M", "lsu",
+                                {"out": (8, 512), "in": (8, 256)},
+                                {"out": 0.0, "in": pace}, "kernel", ("in",), burst))
     elif sweep == "knee":
         # swap-in pace just below the link rate: where does the cost jump?
         for pace in (30.0, 36.0, 40.0, 44.0, 46.0, 48.0, 50.0, 0.0):
@@ -177,11 +184,14 @@ def main():
         for po, pi in ((20.0, 30.0), (25.0, 25.0), (30.0, 30.0), (15.0, 40.0)):
             configs.append(("lsu_duplex", "lsu", {"out": (8, 512), "in": (148, 32)},
                             {"out": po, "in": pi}, "kernel", ("out", "in")))
-    for label, path, ctas, pace, impl, dirs in configs:
+    for cfg in configs:
+        label, path, ctas, pace, impl, dirs = cfg[:6]
+        burst = cfg[6] if len(cfg) > 6 else 0
         for d in ("out", "in"):
             dp.set_path(d, path, 16384 if path == "bulk" else 0, 4 if path == "bulk" else 0)
             dp.set_launch(d, ctas[d][0], ctas[d][1] if path == "lsu" else 0)
             dp.set_pace(d, pace[d])
+            dp.set_pace_burst(d, burst)
         torch.cuda.synchronize()
         t = {}
         moved = {}
