@@ -58,6 +58,47 @@ def token_segments(spans, extents_of, block_tokens: int) -> np.ndarray:
     return np.asarray(rows, dtype=np.int64).reshape(-1, 4)
 
 
+def swap_rate_summary(iv: dict) -> dict:
+    """Per direction, from device intervals [(start_ms, end_ms, bytes)]: GB/s
+    while busy; transfers that ran alone (< 10% overlapped by the other
+    direction) vs those that overlapped it (> 90%: host-link duplex); plans
+    of >= 32 MiB vs smaller ones (fixed cost per launch)."""
+    def merged(xs):
+        out = []
+        for a, b, _ in sorted(xs):
+            if out and a <= out[-1][1]:
+                out[-1][1] = max(out[-1][1], b)
+            else:
+                out.append([a, b])
+        return out
+
+    def rate(xs):
+        t = sum(b - a for a, b, _ in xs)
+        return round(sum(n for *_, n in xs) / (t * 1e-3) / 1e9, 2) if t > 0 else None
+
+    res = {}
+    for d, o in (("out", "in"), ("in", "out")):
+        xs, other = iv.get(d, []), merged(iv.get(o, []))
+        alone, duplex = [], []
+        for a, b, n in xs:
+            ov = sum(max(0.0, min(b, y) - max(a, x)) for x, y in other)
+            if b > a and ov / (b - a) < 0.1:
+                alone.append((a, b, n))
+            elif b > a and ov / (b - a) > 0.9:
+                duplex.append((a, b, n))
+        big = [x for x in xs if x[2] >= 32 << 20]
+        small = [x for x in xs if x[2] < 32 << 20]
+        res[d] = {"gib": round(sum(n for *_, n in xs) / 2**30, 2),
+                  "transfers": len(xs), "gbs_while_busy": rate(xs),
+                  "gbs_alone": rate(alone), "transfers_alone": len(alone),
+                  "gbs_overlapping_other_direction": rate(duplex),
+                  "transfers_overlapping": len(duplex),
+                  "gbs_plans_ge_32mib": rate(big), "gbs_plans_lt_32mib": rate(small),
+                  "mean_plan_mib": round(sum(n for *_, n in xs) / len(xs) / 2**20, 2)
+                  if xs else None}
+    return res
+
+
 class Runtime:
     def __init__(self, geometry: KVGeometry, gpu_blocks: int, cpu_blocks: int,
                  device="cuda:0", copy_impl: str = "kernel", write_kv: bool = True,
@@ -203,9 +244,7 @@ class Runtime:
 
     def swap_rates(self) -> dict:
         """Swap GB/s while a transfer of each direction executes (needs
-        timing=True), and why it is what it is: transfers that ran alone vs
-        those that overlapped the other direction (host-link duplex), and
-        small vs large plans (fixed cost per launch)."""
+        timing=True), and why it is what it is (swap_rate_summary)."""
         recs = [r for r in self.executor.history if r.nbytes and r.start_event is not None]
         if not recs:
             return {}
@@ -215,41 +254,7 @@ class Runtime:
         for r in recs:
             iv[r.direction].append((ref.elapsed_time(r.start_event), ref.elapsed_time(r.event),
                                     r.nbytes + r.refresh_bytes))
-
-        def merged(xs):
-            out = []
-            for a, b, _ in sorted(xs):
-                if out and a <= out[-1][1]:
-                    out[-1][1] = max(out[-1][1], b)
-                else:
-                    out.append([a, b])
-            return out
-
-        def rate(xs):
-            t = sum(b - a for a, b, _ in xs)
-            return round(sum(n for *_, n in xs) / (t * 1e-3) / 1e9, 2) if t > 0 else None
-
-        res = {}
-        for d, o in (("out", "in"), ("in", "out")):
-            xs, other = iv[d], merged(iv[o])
-            alone, duplex = [], []
-            for a, b, n in xs:
-                ov = sum(max(0.0, min(b, y) - max(a, x)) for x, y in other)
-                if b > a and ov / (b - a) < 0.1:
-                    alone.append((a, b, n))
-                elif b > a and ov / (b - a) > 0.9:
-                    duplex.append((a, b, n))
-            big = [x for x in xs if x[2] >= 32 << 20]
-            small = [x for x in xs if x[2] < 32 << 20]
-            res[d] = {"gib": round(sum(n for *_, n in xs) / 2**30, 2),
-                      "transfers": len(xs), "gbs_while_busy": rate(xs),
-                      "gbs_alone": rate(alone), "transfers_alone": len(alone),
-                      "gbs_overlapping_other_direction": rate(duplex),
-                      "transfers_overlapping": len(duplex),
-                      "gbs_plans_ge_32mib": rate(big), "gbs_plans_lt_32mib": rate(small),
-                      "mean_plan_mib": round(sum(n for *_, n in xs) / len(xs) / 2**20, 2)
-                      if xs else None}
-        return res
+        return swap_rate_summary(iv)
 
     def close(self) -> None:
         self.synchronize()

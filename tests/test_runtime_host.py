@@ -50,3 +50,22 @@ def test_empty_and_overflowing_spans():
     assert token_segments([(0, 5, 5)], tables.__getitem__, 16).shape == (0, 4)
     with pytest.raises(IndexError):
         token_segments([(0, 0, 33)], tables.__getitem__, 16)
+
+
+def test_swap_rate_summary_splits_alone_duplex_and_plan_size():
+    from paper_2411_18424_b200.runtime import swap_rate_summary
+
+    mib = 1 << 20
+    iv = {  # (start ms, end ms, bytes) on the device timeline
+        "out": [(0.0, 1.0, 50 * mib), (10.0, 12.0, 100 * mib)],
+        "in": [(2.0, 3.0, 40 * mib),          # alone
+               (10.0, 11.0, 36 * mib),        # fully inside the second swap-out
+               (20.0, 20.1, 4 * mib)],        # small plan, alone
+    }
+    r = swap_rate_summary(iv)
+    assert r["in"]["transfers"] == 3 and r["in"]["transfers_alone"] == 2
+    assert r["in"]["transfers_overlapping"] == 1
+    assert r["in"]["gbs_overlapping_other_direction"] == round(36 * mib / 1e-3 / 1e9, 2)
+    assert abs(r["in"]["gbs_plans_lt_32mib"] - 4 * mib / 0.1e-3 / 1e9) < 0.01
+    assert r["out"]["transfers_alone"] == 1  # the first swap-out ran alone
+    assert r["out"]["gbs_while_busy"] == round(150 * mib / 3e-3 / 1e9, 2)
