@@ -55,3 +55,18 @@ def test_reference_arm_plans_are_the_gpu_arms_plans():
         ref = bench.make_plans(g, 0, runs=random_runs, pair=table_to_ops)
         for a, b in zip(ours, ref):
             assert (a == b).all()
+
+
+def test_control_plane_cost_times_each_hot_call():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    ours = bench.control_plane_cost("ours")
+    for k in ("plan_swap_out", "plan_swap_in", "allocate", "dispatch"):
+        assert ours[f"{k}_calls"] > 0 and ours[f"{k}_us"] > 0
+    assert ours["iterations"] > 1000 and ours["iter_us"] > 0
+    ref = bench.control_plane_cost("reference")
+    if "unavailable" not in ref:  # baseline/_ref installed: same trace, same call counts
+        for k in ("plan_swap_out", "plan_swap_in", "allocate", "dispatch"):
+            assert ref[f"{k}_calls"] == ours[f"{k}_calls"]
+        assert ref["iterations"] == ours["iterations"]
