@@ -407,7 +407,7 @@ def run_ours(args, geo):
     import torch.distributed as dist
 
     from paper_2411_18424_b200.dataplane import (HostKVPool, PagedKVCache, SwapDataPlane,
-                                                 host_link_info, numa_nodes)
+                                                 host_link_info, numa_nodes, pcie_switch_groups)
 
     rank, world, local = dist_env()
     if not torch.cuda.is_available():
@@ -546,9 +546,16 @@ def run_ours(args, geo):
             trace[name] = run_trace(args, geo, dev, name)
 
     root_ports = {lk["root_port"] for lk in links if lk.get("root_port")}
-    # Ranks behind one root port share its link: the aggregate roofline is the
-    # smaller of one link per rank and one per distinct root port.
-    link_cap = PCIE_GEN5_X16_GBS * (min(world, len(root_ports)) if root_ports else world)
+    # GPUs behind one PCIe switch share its uplink (nvidia-smi topo -mp, PCIe only)
+    switches = pcie_switch_groups(world) if world > 1 and rank == 0 else {}
+    # Ranks behind one root port (or switch) share its link: the aggregate
+    # roofline is the smaller of one link per rank and one per shared port.
+    if root_ports:
+        link_cap = PCIE_GEN5_X16_GBS * min(world, len(root_ports))
+    elif switches.get("groups"):
+        link_cap = PCIE_GEN5_X16_GBS * len(switches["groups"])
+    else:
+        link_cap = PCIE_GEN5_X16_GBS * world
 
     barrier()
     cpu = None
@@ -584,6 +591,8 @@ def run_ours(args, geo):
                                        "frac": round(value / (world * PCIE_GEN5_X16_GBS), 4),
                                        "root_ports": len(root_ports) or None,
                                        "topology_cap_gbs": link_cap,
+                                       "pcie_switch_groups": switches.get("groups"),
+                                       "pcie_matrix": switches.get("matrix"),
                                        "frac_of_topology": round(value / link_cap, 4),
                                        "ce_all_ranks_concurrent_gbs": ce_sum,
                                        "ce_per_rank_gbs": ce_all},

@@ -126,6 +126,54 @@ def host_link_info(device=None) -> dict:
     return info
 
 
+def pcie_switch_groups(n: int, text: Optional[str] = None) -> dict:
+    """GPUs 0..n-1 grouped by shared PCIe switch, from `nvidia-smi topo -mp`
+    (the PCIe-only matrix: NVLink would hide the host-link topology).  GPUs
+    whose path is PIX / PXB (through PCIe switches only) share a switch's
+    uplink to the host, so their swaps share one host link.  Returns
+    {"groups": [[gpu, ...], ...], "matrix": {"i-j": relation}} or {} when
+    the matrix is unavailable."""
+    if text is None:
+        import subprocess
+        try:
+            text = subprocess.run(["nvidia-smi", "topo", "-mp"], capture_output=True, text=True,
+                                  timeout=20).stdout
+        except (OSError, subprocess.SubprocessError):
+            return {}
+    rows = [ln.split() for ln in text.splitlines() if ln.strip()]
+    head = next((r for r in rows if r and r[0].startswith("GPU") and len(r) > 1
+                 and r[1].startswith("GPU")), None)
+    if head is None:  # the header row starts with the first column name
+        head = next((r for r in rows if "GPU0" in r and not r[0].startswith("GPU0")), None)
+    if head is None:
+        return {}
+    cols = [c for c in head if c.startswith("GPU") and c[3:].isdigit()]
+    rel = {}
+    for r in rows:
+        if r and r[0] in cols:
+            i = int(r[0][3:])
+            for c, v in zip(cols, r[1:1 + len(cols)]):
+                j = int(c[3:])
+                if i < n and j < n and i != j:
+                    rel[(min(i, j), max(i, j))] = v
+    parent = list(range(n))
+
+    def find(x):
+        while parent[x] != x:
+            parent[x] = parent[parent[x]]
+            x = parent[x]
+        return x
+
+    for (i, j), v in rel.items():
+        if v in ("PIX", "PXB"):
+            parent[find(i)] = find(j)
+    groups: dict = {}
+    for g in range(n):
+        groups.setdefault(find(g), []).append(g)
+    return {"groups": sorted(groups.values()),
+            "matrix": {f"{i}-{j}": v for (i, j), v in sorted(rel.items())}}
+
+
 def gpu_numa_node(device: Union[int, str, torch.device, None]) -> int:
     """NUMA node of the GPU's PCIe root (sysfs), or -1 when unknown.  Each
     rank's swap space belongs on its own GPU's socket: host-link traffic then

@@ -69,3 +69,18 @@ def test_swap_rate_summary_splits_alone_duplex_and_plan_size():
     assert abs(r["in"]["gbs_plans_lt_32mib"] - 4 * mib / 0.1e-3 / 1e9) < 0.01
     assert r["out"]["transfers_alone"] == 1  # the first swap-out ran alone
     assert r["out"]["gbs_while_busy"] == round(150 * mib / 3e-3 / 1e9, 2)
+
+
+def test_pcie_switch_groups_from_the_pcie_only_topology_matrix():
+    from paper_2411_18424_b200.dataplane import pcie_switch_groups
+
+    txt = ("\tGPU0\tGPU1\tGPU2\tGPU3\tNIC0\tCPU Affinity\tNUMA Affinity\tGPU NUMA ID\n"
+           "GPU0\t X \tPIX\tNODE\tSYS\tPXB\t0-55\t0\t\tN/A\n"
+           "GPU1\tPIX\t X \tNODE\tSYS\tPXB\t0-55\t0\t\tN/A\n"
+           "GPU2\tNODE\tNODE\t X \tSYS\tNODE\t0-55\t0\t\tN/A\n"
+           "GPU3\tSYS\tSYS\tSYS\t X \tSYS\t56-111\t1\t\tN/A\n")
+    got = pcie_switch_groups(4, txt)
+    assert got["groups"] == [[0, 1], [2], [3]]  # GPU0/1 share a switch uplink
+    assert got["matrix"]["0-2"] == "NODE"
+    assert pcie_switch_groups(2, txt)["groups"] == [[0, 1]]
+    assert pcie_switch_groups(2, "no matrix here") == {}
