@@ -196,6 +196,9 @@ class LiveStats:
             return float(bx[:, 0].sum() / max(1e-9, pred.sum()) - 1.0)
 
         point = stall(q, b)
+        coef, *_ = np.linalg.lstsq(design(q), q[:, 0], rcond=None)
+        resid = q[:, 0] - design(q) @ coef
+        r2 = 1.0 - float(resid.var()) / max(1e-12, float(q[:, 0].var()))
         rng = np.random.default_rng(seed)
         draws = [stall(q[rng.integers(0, len(q), len(q))], b[rng.integers(0, len(b), len(b))])
                  for _ in range(boot)]
@@ -203,7 +206,9 @@ class LiveStats:
         return {"stall": round(point, 4), "ci95": [round(float(lo), 4), round(float(hi), 4)],
                 "busy_iterations": int(len(b)), "quiet_iterations": int(len(q)),
                 "layered_iterations": int(sum(1 for x in self.samples if x[4])),
-                "busy_means": self.classified}
+                "busy_means": self.classified,
+                "quiet_fit_r2": round(r2, 4),
+                "quiet_fit_resid_pct": round(float(np.abs(resid).mean() / q[:, 0].mean()) * 100, 2)}
 
 
 class RankAgreement:
