@@ -790,7 +790,7 @@ def run_trace(args, geo, dev, name):
 
 
 def serving_interference(dp, dev, s, sm_partition: int = 0, policy: str = "latency",
-                         layers: int = 32):
+                         layers: int = 32, graph: bool = True):
     """Swap-induced decode stall, measured: 2 ms HBM-streaming decode steps
     (each `layers` per-layer kernels, as the live engine runs them) on a
     high-priority stream while a 2 GiB swap runs, per direction and both at
@@ -820,12 +820,26 @@ def serving_interference(dp, dev, s, sm_partition: int = 0, policy: str = "laten
     ops_in[:, 2] += hp
     nbytes = n * dp.geometry.block_bytes
 
+    # the decode step as one CUDA graph, as the live engine and serving
+    # engines launch it (DecodeGraph); graph=False: kernel by kernel
+    g = None
+    if graph:
+        from paper_2411_18424_b200.live import DecodeGraph
+        g = DecodeGraph(dev, marks=0)
+        gs = g.begin()
+        for _ in range(layers):
+            dec.launch_us(gs, 2000.0 / layers)
+        g.end()
+
     def steps(k):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
         evs[0].record(comp)
         for i in range(k):
-            for _ in range(layers):
-                dec.launch_us(comp, 2000.0 / layers)
+            if g is not None:
+                g.launch(comp)
+            else:
+                for _ in range(layers):
+                    dec.launch_us(comp, 2000.0 / layers)
             evs[i + 1].record(comp)
         return evs
 
@@ -844,7 +858,8 @@ def serving_interference(dp, dev, s, sm_partition: int = 0, policy: str = "laten
     dp.set_budget(pol["budget"])
     dp.set_budget_priority(pol.get("priority"))
     out = {"policy": policy, "sm_partition": sms, "decode_step_solo_ms": round(solo, 3),
-           "decode_kernels_per_step": layers, "runs": {}}
+           "decode_kernels_per_step": layers,
+           "decode_launch": "cuda_graph" if g is not None else "stream", "runs": {}}
     for name, dirs in (("out", ("out",)), ("in", ("in",)), ("duplex", ("out", "in"))):
         torch.cuda.synchronize()
         t = {}
@@ -872,6 +887,8 @@ def serving_interference(dp, dev, s, sm_partition: int = 0, policy: str = "laten
         dp.set_budget_share(d, 0.0)
     dp.set_budget(0.0)
     dp.set_budget_priority(None)
+    if g is not None:
+        g.close()
     del dec
     return out
 

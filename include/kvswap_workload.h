@@ -39,6 +39,44 @@ int kvs_stream_read(int device, uint64_t stream, const void* buf, size_t buf_byt
  * differing 32-bit words to *mismatch (device memory).  Word w of plane p, K/V kv of
  * token t of request r is t*0x01000193 + r*0x5BD1E995 + p*0x9E3779B1 +
  * kv*0x7F4A7C15 + w (mod 2^32). */
+/* kvs_stream_read with launch flags: KVS_DECODE_PDL launches with
+ * programmatic stream serialization and triggers the next kernel's launch at
+ * entry (a CUDA-graph / PDL decode, as serving engines chain a model's
+ * per-layer kernels); KVS_DECODE_WAIT then waits (griddepcontrol.wait) for
+ * the previous kernel's completion before reading — a real layer-to-layer
+ * dependency, so only launch latency and ramp overlap, not the work. */
+#define KVS_DECODE_PDL 1
+#define KVS_DECODE_WAIT 2
+int kvs_stream_read_ex(int device, uint64_t stream, const void* buf, size_t buf_bytes,
+                       size_t bytes, int ctas, void* sink, int flags);
+
+/* Decode step as a CUDA graph (how serving engines launch a model's
+ * per-layer decode kernels).  Stream-launched kernels fetch their commands
+ * from host memory over the same PCIe link a swap-in saturates, so every
+ * launch waits behind the swap's reads (a 32-layer step pays
+ * +20% under a full-rate swap-in stream-launched, +9% graph-launched).
+ *
+ * kvs_graph_begin starts capturing on the graph's private stream
+ * (kvs_graph_stream); launch decode kernels (kvs_stream_read(_ex),
+ * kvs_kv_tokens), plane-flag waits (kvs_wait_flag) and timing marks
+ * (kvs_graph_mark: event `slot` recorded as a graph node) on it;
+ * kvs_graph_end ends the capture and updates the executable graph in place
+ * (cudaGraphExecUpdate, *how = 1) or instantiates it (*how = 2) when the
+ * step's structure changed; kvs_graph_launch runs it on `stream`.
+ * kvs_graph_elapsed reads the time between two marks after the launch
+ * completed. */
+typedef struct KvsGraph KvsGraph;
+int kvs_graph_create(int device, int n_marks, KvsGraph** out);
+int kvs_graph_destroy(KvsGraph* g);
+int kvs_graph_stream(KvsGraph* g, uint64_t* stream);
+int kvs_graph_begin(KvsGraph* g);
+int kvs_graph_mark(KvsGraph* g, int slot);
+int kvs_graph_end(KvsGraph* g, int* how);
+int kvs_graph_launch(KvsGraph* g, uint64_t stream);
+int kvs_graph_elapsed(KvsGraph* g, int slot_a, int slot_b, float* ms);
+/* instantiations, in-place updates, launches */
+int kvs_graph_stats(KvsGraph* g, int64_t* out3);
+
 typedef struct KvsHandle KvsHandle;
 int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_t n_segs,
                   int32_t block_tokens, int32_t plane_lo, int32_t plane_hi, uint64_t stream,

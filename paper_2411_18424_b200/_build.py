@@ -73,6 +73,34 @@ def build_oracle(force: bool = False) -> Path:
     return out
 
 
+def build_kvctrl(force: bool = False) -> Path:
+    """Compile the native control plane (host C++): the C ABI library
+    PKG/libkvctrl.so (csrc/ctrlplane.cpp, include/kvctrl.h) and the CPython
+    extension PKG/_kvctrl<EXT_SUFFIX> (csrc/kvctrl_py.cpp, same C++)."""
+    import sysconfig
+
+    src = PKG / "csrc" / "ctrlplane.cpp"
+    py_src = PKG / "csrc" / "kvctrl_py.cpp"
+    hdr = ROOT / "include" / "kvctrl.h"
+    lib = PKG / "libkvctrl.so"
+    ext = PKG / ("_kvctrl" + sysconfig.get_config_var("EXT_SUFFIX"))
+    base = ["g++", "-O3", "-std=c++17", "-Wall", "-Wextra", "-shared", "-fPIC",
+            "-I", str(ROOT / "include")]
+    jobs = [(lib, [src], base),
+            (ext, [py_src], base + ["-I", sysconfig.get_paths()["include"]])]
+    for out, srcs, cmd in jobs:
+        if not force and not _stale(out, src, py_src, hdr, Path(__file__)):
+            continue
+        tmp = out.with_name(out.name + ".tmp")
+        res = subprocess.run(cmd + ["-o", str(tmp)] + [str(x) for x in srcs],
+                             capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"g++ failed ({res.returncode}):\n{res.stderr}")
+        tmp.replace(out)
+    return ext
+
+
 def build_all(force: bool = False) -> None:
     build_kvswap(force=force)
+    build_kvctrl(force=force)
     build_oracle(force=force)

@@ -63,6 +63,10 @@ EXPORTED_SYMBOLS = (
     "kvs_host_free",
     "kvs_sm_partition",
     "kvs_stream_read",  # include/kvswap_workload.h
+    "kvs_stream_read_ex",  # include/kvswap_workload.h
+    "kvs_graph_create", "kvs_graph_destroy", "kvs_graph_stream", "kvs_graph_begin",
+    "kvs_graph_mark", "kvs_graph_end", "kvs_graph_launch", "kvs_graph_elapsed",
+    "kvs_graph_stats",  # include/kvswap_workload.h
     "kvs_kv_tokens",  # include/kvswap_workload.h
 )
 
@@ -165,6 +169,27 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_stream_read.restype = c.c_int
     lib.kvs_stream_read.argtypes = [c.c_int, c.c_uint64, c.c_void_p, c.c_size_t, c.c_size_t,
                                     c.c_int, c.c_void_p]
+    lib.kvs_stream_read_ex.restype = c.c_int
+    lib.kvs_stream_read_ex.argtypes = [c.c_int, c.c_uint64, c.c_void_p, c.c_size_t, c.c_size_t,
+                                       c.c_int, c.c_void_p, c.c_int]
+    lib.kvs_graph_create.restype = c.c_int
+    lib.kvs_graph_create.argtypes = [c.c_int, c.c_int, c.POINTER(c.c_void_p)]
+    lib.kvs_graph_destroy.restype = c.c_int
+    lib.kvs_graph_destroy.argtypes = [c.c_void_p]
+    lib.kvs_graph_stream.restype = c.c_int
+    lib.kvs_graph_stream.argtypes = [c.c_void_p, c.POINTER(c.c_uint64)]
+    lib.kvs_graph_begin.restype = c.c_int
+    lib.kvs_graph_begin.argtypes = [c.c_void_p]
+    lib.kvs_graph_mark.restype = c.c_int
+    lib.kvs_graph_mark.argtypes = [c.c_void_p, c.c_int]
+    lib.kvs_graph_end.restype = c.c_int
+    lib.kvs_graph_end.argtypes = [c.c_void_p, c.POINTER(c.c_int)]
+    lib.kvs_graph_launch.restype = c.c_int
+    lib.kvs_graph_launch.argtypes = [c.c_void_p, c.c_uint64]
+    lib.kvs_graph_elapsed.restype = c.c_int
+    lib.kvs_graph_elapsed.argtypes = [c.c_void_p, c.c_int, c.c_int, c.POINTER(c.c_float)]
+    lib.kvs_graph_stats.restype = c.c_int
+    lib.kvs_graph_stats.argtypes = [c.c_void_p, c.POINTER(c.c_int64)]
     lib.kvs_kv_tokens.restype = c.c_int
     lib.kvs_kv_tokens.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_int32,
                                   c.c_int32, c.c_int32, c.c_uint64, c.c_void_p]

@@ -1132,7 +1132,13 @@ namespace {
 __global__ void __launch_bounds__(512) kvs_stream_read_kernel(const int4* __restrict__ buf,
                                                               uint64_t buf_vecs,
                                                               uint64_t total_vecs,
-                                                              int4* sink) {
+                                                              int4* sink, int flags) {
+  // Programmatic dependent launch (KVS_DECODE_PDL): let the next layer's
+  // kernel be scheduled now; with KVS_DECODE_WAIT, consume only after the
+  // previous layer's kernel completed and its writes are visible (a real
+  // layer-to-layer data dependency).
+  if (flags & KVS_DECODE_PDL) asm volatile("griddepcontrol.launch_dependents;");
+  if (flags & KVS_DECODE_WAIT) asm volatile("griddepcontrol.wait;" ::: "memory");
   const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t step = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   // Power-of-two buffers wrap with a mask; others with a (slow) modulo.
@@ -1165,7 +1171,9 @@ __global__ void __launch_bounds__(512) kvs_stream_read_tiled_kernel(const int4* 
                                                                     uint64_t buf_vecs,
                                                                     uint64_t total_vecs,
                                                                     uint64_t tile_vecs,
-                                                                    int4* sink) {
+                                                                    int4* sink, int flags) {
+  if (flags & KVS_DECODE_PDL) asm volatile("griddepcontrol.launch_dependents;");
+  if (flags & KVS_DECODE_WAIT) asm volatile("griddepcontrol.wait;" ::: "memory");
   const bool pow2 = (buf_vecs & (buf_vecs - 1)) == 0;
   const uint64_t mask = buf_vecs - 1;
   const uint64_t lo = blockIdx.x * tile_vecs;
@@ -1192,36 +1200,183 @@ __global__ void __launch_bounds__(512) kvs_stream_read_tiled_kernel(const int4* 
 
 }  // namespace
 
-extern "C" int kvs_stream_read(int device, uint64_t stream, const void* buf, size_t buf_bytes,
-                               size_t bytes, int ctas, void* sink) {
-  if (buf == nullptr || sink == nullptr || buf_bytes < 16 || bytes == 0 || device < 0)
-    return KVS_ERR_INVALID;
-  if (ctas < 0) {  // tiled: -ctas KiB per CTA
-    if (reinterpret_cast<uintptr_t>(buf) % 16 || reinterpret_cast<uintptr_t>(sink) % 16)
-      return KVS_ERR_ALIGN;
-    int rc = cuda_rc(cudaSetDevice(device));
-    if (rc) return rc;
-    const uint64_t tile_vecs = static_cast<uint64_t>(-static_cast<int64_t>(ctas)) * 1024 / 16;
-    const uint64_t total = bytes / 16;
-    const uint64_t grid = (total + tile_vecs - 1) / tile_vecs;
-    if (grid > 0x7FFFFFFFull) return KVS_ERR_RANGE;
-    kvs_stream_read_tiled_kernel<<<static_cast<unsigned>(grid), 512, 0,
-                                   reinterpret_cast<cudaStream_t>(stream)>>>(
-        static_cast<const int4*>(buf), buf_bytes / 16, total, tile_vecs, static_cast<int4*>(sink));
-    return cuda_rc(cudaGetLastError());
+template <typename... KArgs, typename... Args>
+int launch_decode(void (*kernel)(KArgs...), unsigned grid, cudaStream_t st, int flags,
+                  Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(512);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  if (flags & KVS_DECODE_PDL) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
   }
+  return cuda_rc(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
+extern "C" int kvs_stream_read_ex(int device, uint64_t stream, const void* buf, size_t buf_bytes,
+                                  size_t bytes, int ctas, void* sink, int flags) {
+  if (buf == nullptr || sink == nullptr || buf_bytes < 16 || bytes == 0 || device < 0 ||
+      (flags & ~(KVS_DECODE_PDL | KVS_DECODE_WAIT)))
+    return KVS_ERR_INVALID;
   if (reinterpret_cast<uintptr_t>(buf) % 16 || reinterpret_cast<uintptr_t>(sink) % 16)
     return KVS_ERR_ALIGN;
   int rc = cuda_rc(cudaSetDevice(device));
   if (rc) return rc;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (ctas < 0) {  // tiled: -ctas KiB per CTA
+    const uint64_t tile_vecs = static_cast<uint64_t>(-static_cast<int64_t>(ctas)) * 1024 / 16;
+    const uint64_t total = bytes / 16;
+    const uint64_t grid = (total + tile_vecs - 1) / tile_vecs;
+    if (grid > 0x7FFFFFFFull) return KVS_ERR_RANGE;
+    return launch_decode(kvs_stream_read_tiled_kernel, static_cast<unsigned>(grid), st, flags,
+                         static_cast<const int4*>(buf), buf_bytes / 16, total, tile_vecs,
+                         static_cast<int4*>(sink), flags);
+  }
   if (ctas == 0) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     ctas = 2 * sms;
   }
-  kvs_stream_read_kernel<<<ctas, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      static_cast<const int4*>(buf), buf_bytes / 16, bytes / 16, static_cast<int4*>(sink));
-  return cuda_rc(cudaGetLastError());
+  return launch_decode(kvs_stream_read_kernel, static_cast<unsigned>(ctas), st, flags,
+                       static_cast<const int4*>(buf), buf_bytes / 16, bytes / 16,
+                       static_cast<int4*>(sink), flags);
+}
+
+extern "C" int kvs_stream_read(int device, uint64_t stream, const void* buf, size_t buf_bytes,
+                               size_t bytes, int ctas, void* sink) {
+  return kvs_stream_read_ex(device, stream, buf, buf_bytes, bytes, ctas, sink, 0);
+}
+
+// ---------------------------------------------------------------------------
+// Decode step as a CUDA graph (include/kvswap_workload.h, kvs_graph_*).
+// ---------------------------------------------------------------------------
+struct KvsGraph {
+  int device = 0;
+  cudaStream_t cap = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaEvent_t> marks;
+  bool capturing = false;
+  int64_t instantiations = 0, updates = 0, launches = 0;
+};
+
+extern "C" int kvs_graph_create(int device, int n_marks, KvsGraph** out) {
+  if (out == nullptr || device < 0 || n_marks < 0 || n_marks > 4096) return KVS_ERR_INVALID;
+  int rc = cuda_rc(cudaSetDevice(device));
+  if (rc) return rc;
+  auto* g = new KvsGraph();
+  g->device = device;
+  rc = cuda_rc(cudaStreamCreateWithFlags(&g->cap, cudaStreamNonBlocking));
+  for (int i = 0; i < n_marks && rc == 0; ++i) {
+    cudaEvent_t e = nullptr;
+    rc = cuda_rc(cudaEventCreate(&e));
+    if (rc == 0) g->marks.push_back(e);
+  }
+  if (rc) {
+    kvs_graph_destroy(g);
+    return rc;
+  }
+  *out = g;
+  return KVS_OK;
+}
+
+extern "C" int kvs_graph_destroy(KvsGraph* g) {
+  if (g == nullptr) return KVS_OK;
+  cudaSetDevice(g->device);
+  if (g->capturing) {
+    cudaGraph_t dead = nullptr;
+    cudaStreamEndCapture(g->cap, &dead);
+    if (dead) cudaGraphDestroy(dead);
+  }
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  for (cudaEvent_t e : g->marks) cudaEventDestroy(e);
+  if (g->cap) cudaStreamDestroy(g->cap);
+  delete g;
+  return KVS_OK;
+}
+
+extern "C" int kvs_graph_stream(KvsGraph* g, uint64_t* stream) {
+  if (g == nullptr || stream == nullptr) return KVS_ERR_INVALID;
+  *stream = reinterpret_cast<uint64_t>(g->cap);
+  return KVS_OK;
+}
+
+extern "C" int kvs_graph_begin(KvsGraph* g) {
+  if (g == nullptr || g->capturing) return KVS_ERR_INVALID;
+  int rc = cuda_rc(cudaSetDevice(g->device));
+  if (rc) return rc;
+  rc = cuda_rc(cudaStreamBeginCapture(g->cap, cudaStreamCaptureModeThreadLocal));
+  if (rc == 0) g->capturing = true;
+  return rc;
+}
+
+extern "C" int kvs_graph_mark(KvsGraph* g, int slot) {
+  if (g == nullptr || !g->capturing || slot < 0 || slot >= static_cast<int>(g->marks.size()))
+    return KVS_ERR_INVALID;
+  return cuda_rc(cudaEventRecordWithFlags(g->marks[slot], g->cap, cudaEventRecordExternal));
+}
+
+extern "C" int kvs_graph_end(KvsGraph* g, int* how) {
+  if (g == nullptr || how == nullptr || !g->capturing) return KVS_ERR_INVALID;
+  int rc = cuda_rc(cudaSetDevice(g->device));
+  if (rc) return rc;
+  cudaGraph_t graph = nullptr;
+  g->capturing = false;
+  rc = cuda_rc(cudaStreamEndCapture(g->cap, &graph));
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  *how = 0;
+  if (g->exec != nullptr) {
+    cudaGraphExecUpdateResultInfo info{};
+    if (cudaGraphExecUpdate(g->exec, graph, &info) == cudaSuccess) {
+      *how = 1;
+      ++g->updates;
+    } else {
+      cudaGetLastError();  // clear the update failure; re-instantiate below
+      cudaGraphExecDestroy(g->exec);
+      g->exec = nullptr;
+    }
+  }
+  if (g->exec == nullptr) {
+    rc = cuda_rc(cudaGraphInstantiate(&g->exec, graph, 0));
+    if (rc == 0) {
+      *how = 2;
+      ++g->instantiations;
+    } else {
+      g->exec = nullptr;
+    }
+  }
+  cudaGraphDestroy(graph);
+  return rc;
+}
+
+extern "C" int kvs_graph_launch(KvsGraph* g, uint64_t stream) {
+  if (g == nullptr || g->exec == nullptr || g->capturing) return KVS_ERR_INVALID;
+  int rc = cuda_rc(cudaSetDevice(g->device));
+  if (rc) return rc;
+  rc = cuda_rc(cudaGraphLaunch(g->exec, reinterpret_cast<cudaStream_t>(stream)));
+  if (rc == 0) ++g->launches;
+  return rc;
+}
+
+extern "C" int kvs_graph_elapsed(KvsGraph* g, int slot_a, int slot_b, float* ms) {
+  const int n = g ? static_cast<int>(g->marks.size()) : 0;
+  if (g == nullptr || ms == nullptr || slot_a < 0 || slot_b < 0 || slot_a >= n || slot_b >= n)
+    return KVS_ERR_INVALID;
+  return cuda_rc(cudaEventElapsedTime(ms, g->marks[slot_a], g->marks[slot_b]));
+}
+
+extern "C" int kvs_graph_stats(KvsGraph* g, int64_t* out3) {
+  if (g == nullptr || out3 == nullptr) return KVS_ERR_INVALID;
+  out3[0] = g->instantiations;
+  out3[1] = g->updates;
+  out3[2] = g->launches;
+  return KVS_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -157,10 +157,12 @@ def import_image(src: Union[str, BinaryIO], store: CpuStore, pool: np.ndarray, r
         if executor is not None:
             executor.host_fence([(g.start, g.length) for g in groups])
         pos = 0
+        segs = []
         for g in groups:
             pool[g.start:g.start + g.length] = data[pos:pos + g.length]
-            copy.segments.append(Segment(pos, pos + g.length, g.id, True))
+            segs.append(Segment(pos, pos + g.length, g.id, True))
             pos += g.length
-    store.copies[req] = copy
+        copy.segments = segs
+    store.copies[req] = copy  # the native store copies it in (native_ctrl._Copies)
     store._track_peak()
-    return copy
+    return store.copy_of(req)

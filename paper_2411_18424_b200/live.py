@@ -93,6 +93,67 @@ class DecodeEmulator:
         return 3 * nbytes / (e0.elapsed_time(e1) * 1e3)
 
 
+class DecodeGraph:
+    """A decode step launched as one CUDA graph (kvs_graph_*, include/
+    kvswap_workload.h), as serving engines launch a model's per-layer decode.
+
+    Each iteration the step is re-captured on the graph's private stream and
+    the executable graph is updated in place (cudaGraphExecUpdate) — the
+    structure is fixed (attention + weight kernel per layer, plane-flag waits
+    in layered steps) while the batch and modeled time change.  Why it
+    matters for the swap path: stream-launched kernels fetch
+    their commands from host memory over the PCIe link a swap-in saturates."""
+
+    def __init__(self, device, marks: int = 160) -> None:
+        self.lib = _lib.load()
+        dev = torch.device(device)
+        idx = dev.index if dev.index is not None else torch.cuda.current_device()
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.kvs_graph_create(idx, marks, ctypes.byref(h)), "kvs_graph_create")
+        self.h = h
+        self.marks = marks
+        st = ctypes.c_uint64()
+        _lib.check(self.lib.kvs_graph_stream(h, ctypes.byref(st)), "kvs_graph_stream")
+        self.stream = torch.cuda.ExternalStream(st.value, device=torch.device("cuda", idx))
+
+    def begin(self) -> torch.cuda.Stream:
+        _lib.check(self.lib.kvs_graph_begin(self.h), "kvs_graph_begin")
+        return self.stream
+
+    def mark(self, slot: int) -> None:
+        _lib.check(self.lib.kvs_graph_mark(self.h, slot), "kvs_graph_mark")
+
+    def end(self) -> int:
+        how = ctypes.c_int()
+        _lib.check(self.lib.kvs_graph_end(self.h, ctypes.byref(how)), "kvs_graph_end")
+        return how.value
+
+    def launch(self, stream) -> None:
+        _lib.check(self.lib.kvs_graph_launch(self.h, int(stream.cuda_stream)), "kvs_graph_launch")
+
+    def elapsed(self, a: int, b: int) -> float:
+        ms = ctypes.c_float()
+        _lib.check(self.lib.kvs_graph_elapsed(self.h, a, b, ctypes.byref(ms)),
+                   "kvs_graph_elapsed")
+        return ms.value
+
+    def stats(self) -> dict:
+        out = (ctypes.c_int64 * 3)()
+        _lib.check(self.lib.kvs_graph_stats(self.h, out), "kvs_graph_stats")
+        return {"instantiations": out[0], "updates": out[1], "launches": out[2]}
+
+    def close(self) -> None:
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.kvs_graph_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self) -> None:  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 @dataclass
 class LiveStats:
     decode_ms: float = 0.0  # measured decode-kernel time (with concurrent swaps)
@@ -259,7 +320,8 @@ class LiveEngine(Engine):
     def __init__(self, config: EngineConfig, conversations, runtime, decode: DecodeEmulator,
                  time_scale: float = 1.0, agreement: Optional[RankAgreement] = None,
                  layered: bool = False, attend: bool = True,
-                 per_layer_decode: bool = True) -> None:
+                 per_layer_decode: bool = True, control_plane: Optional[str] = None,
+                 graph_decode: bool = True) -> None:
         """layered: resumed requests join decode layer by layer (SURVEY §8f
         rank 2).  A swap-in at the head of the swap-in stream whose modeled
         completion falls inside this iteration joins the batch now, and so do
@@ -276,10 +338,14 @@ class LiveEngine(Engine):
         kernel per layer (plane), as a model's layers are — in every
         iteration, so a layered join's per-layer kernels and an ordinary
         step's have the same launch structure and the swap-induced stall
-        compares like with like."""
+        compares like with like.
+
+        graph_decode: the step's kernels (and a layered step's plane-flag
+        waits) are launched as one CUDA graph (DecodeGraph), as serving
+        engines launch decode; False launches them one by one on the stream."""
         if runtime is None:
             raise ValueError("live mode needs a Runtime (real data plane)")
-        super().__init__(config, conversations, runtime=runtime)
+        super().__init__(config, conversations, runtime=runtime, control_plane=control_plane)
         self.decode = decode
         self.time_scale = time_scale
         self.agreement = agreement
@@ -291,6 +357,9 @@ class LiveEngine(Engine):
         self.layered_joins = 0
         self.attend = attend and runtime.write_kv
         self.per_layer_decode = per_layer_decode
+        planes = runtime.geometry.num_planes
+        self.graph = (DecodeGraph(runtime.executor.compute.device, marks=2 * planes + 2)
+                      if graph_decode and per_layer_decode and planes > 1 else None)
         self.live = LiveStats(bytes_per_us=decode.bytes_per_us)
         # per computing iteration: (duration_us, cpu_us, wait_ms, kernel_ms,
         #                           synced, conflict_waits, n_prefill, n_decode)
@@ -544,24 +613,38 @@ class LiveEngine(Engine):
                 t_rt = time.perf_counter()
                 waits_seen = grant_waits + list(ex.last_barrier)
                 swapping = True
-                e0.record(compute)
                 planes = self.runtime.geometry.num_planes
                 kv_b = w_b = 0
                 layer_evs = []
                 segs = self.runtime.read_segments(self, reads) if reads else None
+                g = self.graph
+                st = g.begin() if g is not None else compute
+                if g is None:
+                    e0.record(compute)
                 for layer in range(planes):
                     for dep in layer_deps:
-                        ex.wait_plane(compute, dep, layer)
-                    ea = torch.cuda.Event(enable_timing=True)
-                    ea.record(compute)  # this layer's KV has landed: decode starts
+                        ex.wait_plane(st, dep, layer)
+                    if g is None:
+                        ea = torch.cuda.Event(enable_timing=True)
+                        ea.record(compute)  # this layer's KV has landed: decode starts
+                    else:
+                        g.mark(2 * layer)
                     if reads:
                         kv_b += self.runtime.attend(self, reads, planes=(layer, layer + 1),
-                                                   segs=segs)
+                                                   segs=segs, stream=st)
                     if w_us > 0:
-                        w_b += self.decode.launch_us(compute, w_us / planes)
-                    eb = torch.cuda.Event(enable_timing=True)
-                    eb.record(compute)
-                    layer_evs.append((ea, eb))
+                        w_b += self.decode.launch_us(st, w_us / planes)
+                    if g is None:
+                        eb = torch.cuda.Event(enable_timing=True)
+                        eb.record(compute)
+                        layer_evs.append((ea, eb))
+                    else:
+                        g.mark(2 * layer + 1)
+                        layer_evs.append((2 * layer, 2 * layer + 1))
+                if g is not None:
+                    g.end()
+                    e0.record(compute)
+                    g.launch(compute)
                 e1.record(compute)
                 self.runtime.write(self, spans)
             else:
@@ -575,12 +658,17 @@ class LiveEngine(Engine):
                 if self.per_layer_decode and planes > 1:
                     kv_b = w_b = 0
                     segs = self.runtime.read_segments(self, reads) if reads else None
+                    g = self.graph
+                    st = g.begin() if g is not None else compute
                     for layer in range(planes):
                         if reads:
                             kv_b += self.runtime.attend(self, reads, planes=(layer, layer + 1),
-                                                       segs=segs)
+                                                       segs=segs, stream=st)
                         if w_us > 0:
-                            w_b += self.decode.launch_us(compute, w_us / planes)
+                            w_b += self.decode.launch_us(st, w_us / planes)
+                    if g is not None:
+                        g.end()
+                        g.launch(compute)
                 else:
                     kv_b = self.runtime.attend(self, reads) if reads else 0
                     w_b = self.decode.launch_us(compute, w_us) if w_us > 0 else 0
@@ -599,8 +687,12 @@ class LiveEngine(Engine):
             nominal_ms = (kv_b + w_b) / self.decode.bytes_per_us / 1e3
             # Layered steps include plane-flag waits: their decode sample is
             # the per-layer kernel time, waits excluded.
-            dec_ms = kernel_ms if layer_evs is None else sum(a.elapsed_time(b)
-                                                            for a, b in layer_evs)
+            if layer_evs is None:
+                dec_ms = kernel_ms
+            elif self.graph is not None:
+                dec_ms = sum(self.graph.elapsed(a, b) for a, b in layer_evs)
+            else:
+                dec_ms = sum(a.elapsed_time(b) for a, b in layer_evs)
             self.live.samples.append((dec_ms, kv_b, w_b, swapping, layer_evs is not None,
                                       self._ref_ev.elapsed_time(e0),
                                       self._ref_ev.elapsed_time(e1)))

@@ -184,7 +184,7 @@ class Runtime:
         return self.segments(engine, [(req, 0, lo) for req, lo, _ in spans])
 
     def attend(self, engine, spans, planes: Optional[tuple[int, int]] = None,
-               segs: Optional[np.ndarray] = None) -> int:
+               segs: Optional[np.ndarray] = None, stream=None) -> int:
         """Attention stand-in: read (and check) the resident KV of every
         computing request, tokens [0, lo) of each span, in `planes`; returns
         the bytes read.  Mismatches accumulate on the device (kv_errors())."""
@@ -194,7 +194,7 @@ class Runtime:
             segs = self.read_segments(engine, spans)
         if not len(segs):
             return 0
-        self.dataplane.kv_tokens(1, segs, stream=self.executor.compute,
+        self.dataplane.kv_tokens(1, segs, stream=stream or self.executor.compute,
                                  mismatch_ptr=self._kv_bad.data_ptr(), planes=planes)
         tokens = int((segs[:, 2] - segs[:, 1]).sum())
         n = self.geometry.num_planes if planes is None else planes[1] - planes[0]
@@ -218,7 +218,7 @@ class Runtime:
         segs = self.segments(engine, [(req, 0, valid)])
         with torch.cuda.stream(self.executor.compute):
             self._mismatch.zero_()
-        self.dataplane.kv_tokens(1, segs, stream=self.executor.compute,
+        self.dataplane.kv_tokens(1, segs, stream=stream or self.executor.compute,
                                  mismatch_ptr=self._mismatch.data_ptr())
         self.executor.compute.synchronize()
         bad = int(self._mismatch.item())

@@ -1,0 +1,92 @@
+"""The decode step as a CUDA graph (kvs_graph_*, live.DecodeGraph): captured
+attention (KV check) and weight-stream kernels run with each iteration's
+parameters after an in-place update; plane-flag waits captured in the graph
+hold the step until the flag is published; timing marks are read back."""
+
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
+from paper_2411_18424_b200.geometry import KVGeometry
+from paper_2411_18424_b200.live import DecodeEmulator, DecodeGraph
+
+pytestmark = pytest.mark.gpu
+
+GEO = KVGeometry("tiny-kv", num_layers=4, num_kv_heads=2, head_dim=8)  # 1 KiB chunks
+
+
+def _setup():
+    cache = PagedKVCache(GEO, 64, device="cuda:0")
+    host = HostKVPool(16, GEO.block_bytes)
+    dp = SwapDataPlane(cache, host)
+    return cache, host, dp
+
+
+def test_graph_updates_in_place_and_runs_each_iterations_parameters(cuda_ok):
+    cache, host, dp = _setup()
+    dec = DecodeEmulator("cuda:0", weight_bytes=64 << 20)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda:0")
+    g = DecodeGraph("cuda:0", marks=2 * GEO.num_planes)
+    comp = torch.cuda.Stream()
+    # KV of two requests written on the stream (the ordinary path)
+    segs = np.array([[3, 0, 40, 5], [7, 0, 17, 20]], dtype=np.int64)
+    dp.kv_tokens(0, segs, stream=comp)
+    comp.synchronize()
+    for it in range(4):
+        # each iteration reads a different prefix of the KV (different grid)
+        rd = segs.copy()
+        rd[:, 2] = [40 - 7 * it, 17 - 3 * it]
+        st = g.begin()
+        for layer in range(GEO.num_planes):
+            g.mark(2 * layer)
+            dp.kv_tokens(1, rd, stream=st, mismatch_ptr=bad.data_ptr(), planes=(layer, layer + 1))
+            dec.launch(st, (1 + it) << 20)
+            g.mark(2 * layer + 1)
+        how = g.end()
+        assert how == (2 if it == 0 else 1)  # instantiated once, then updated in place
+        g.launch(comp)
+        comp.synchronize()
+        assert int(bad.item()) == 0
+        assert all(g.elapsed(2 * l, 2 * l + 1) > 0 for l in range(GEO.num_planes))
+    # a corrupted KV word (plane 0, block 5, token 1's K row) is seen by the graph
+    cache.planes[0, 5, 32] += 1
+    st = g.begin()
+    dp.kv_tokens(1, segs, stream=st, mismatch_ptr=bad.data_ptr(), planes=(0, 1))
+    g.end()
+    g.launch(comp)
+    comp.synchronize()
+    assert int(bad.item()) > 0
+    assert g.stats()["launches"] == 5
+    g.close()
+    host.close()
+
+
+def test_plane_flag_waits_are_graph_nodes(cuda_ok):
+    cache, host, dp = _setup()
+    flags = torch.zeros(4, dtype=torch.int32, device="cuda:0")
+    g = DecodeGraph("cuda:0", marks=2)
+    comp = torch.cuda.Stream()
+    segs = np.array([[1, 0, 16, 9]], dtype=np.int64)
+    st = g.begin()
+    dp.wait_flag(st, flags.data_ptr() + 4 * 2, 5)  # waits for flags[2] >= 5
+    g.mark(0)
+    dp.kv_tokens(0, segs, stream=st)  # writes request 1's KV after the wait
+    g.mark(1)
+    g.end()
+    cache.planes.zero_()
+    torch.cuda.synchronize()
+    g.launch(comp)
+    time.sleep(0.05)
+    assert not comp.query()  # parked on the flag
+    assert int(cache.planes.view(torch.int32).abs().sum().item()) == 0
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        flags[2] = 5
+    comp.synchronize()
+    assert int(cache.planes.view(torch.int32).abs().sum().item()) > 0
+    assert g.elapsed(0, 1) > 0
+    g.close()
+    host.close()

@@ -242,3 +242,22 @@ def test_live_engine_flag_ring_wraps(cuda_ok):
     assert rt.executor._seq * 3 > 64  # many more completion words than ring slots
     assert rt.kv_errors() == 0
     rt.close()
+
+
+def test_native_control_plane_drives_real_bytes(cuda_ok):
+    """Engine(control_plane="native"): the C++ pool / store plan every swap of
+    a multi-turn trace; decisions equal the Python control plane's and every
+    swap-in is byte-verified."""
+    convs = generate(WorkloadConfig(num_conversations=12, seed=5, max_context_tokens=2048))
+    cfg = EngineConfig(gpu_pool=PoolConfig(total_blocks=256, initial_group_blocks=60),
+                       trace=PriorityTrace(pattern="random", frequency=0.2, seed=2),
+                       ablation="full", cpu_pool_blocks=2048)
+    reports = {}
+    for cp in ("python", "native"):
+        rt = _runtime(cfg)
+        eng = Engine(cfg, convs, runtime=rt, control_plane=cp)
+        reports[cp] = json.loads(eng.run().to_json())
+        rt.synchronize()
+        assert rt.verified > 0
+        rt.close()
+    assert reports["native"] == reports["python"]

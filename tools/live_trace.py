@@ -39,7 +39,9 @@ def run_one(args, mode, impl, decode, geo):
                  verify=args.verify, timing=True, duplex_policy=args.policy,
                  sm_partition=args.sm_partition, layered_swap_in=args.layered)
     eng = LiveEngine(cfg, generate(wl), rt, decode, layered=args.layered and impl == "kernel",
-                     per_layer_decode=not args.single_kernel_decode)
+                     per_layer_decode=not args.single_kernel_decode,
+                     graph_decode=not args.stream_decode,
+                     control_plane=args.control_plane)
     eng.turn_trace = []
     t0 = time.perf_counter()
     rep = eng.run()
@@ -57,6 +59,9 @@ def run_one(args, mode, impl, decode, geo):
     out = {
         "mode": mode, "copy_impl": impl, "wall_s": round(wall, 2),
         "policy": args.policy, "layered": args.layered, "sm_partition": args.sm_partition,
+        "decode_launch": "cuda_graph" if eng.graph is not None else "stream",
+        "control_plane": args.control_plane,
+        "graph_stats": eng.graph.stats() if eng.graph is not None else None,
         "latency": lat,
         "swap_rates": rt.swap_rates(),
         "report": {k: v for k, v in rep.to_dict().items() if k != "granularity_histogram"},
@@ -101,6 +106,10 @@ def main():
                          "<0 = one CTA per -N KiB tile (block-scheduler balanced)")
     ap.add_argument("--single-kernel-decode", action="store_true",
                     help="one weight-stream kernel per step instead of one per layer")
+    ap.add_argument("--stream-decode", action="store_true",
+                    help="launch the per-layer decode kernels one by one on the stream "
+                         "instead of as one CUDA graph")
+    ap.add_argument("--control-plane", default="python", choices=["python", "native"])
     ap.add_argument("--out", default="gpurun_out/live_trace.json")
     args = ap.parse_args()
     geo = PRESETS[args.model]
