@@ -97,6 +97,12 @@ def parse(argv=None):
                     help="StreamExecutor duplex policy of the headline e2e leg")
     ap.add_argument("--serving-policy", default="serving",
                     help="StreamExecutor duplex policy of the live traces' FastSwitch arm")
+    ap.add_argument("--control-plane", default="native", choices=["native", "python"],
+                    help="live traces: the C++ control plane (native_ctrl) or the Python "
+                         "one (same decisions)")
+    ap.add_argument("--stream-decode", action="store_true",
+                    help="live traces / serving: launch decode kernels one by one instead "
+                         "of as one CUDA graph per step")
     return ap.parse_args(argv)
 
 
@@ -268,7 +274,9 @@ def control_plane_cost(which: str) -> dict:
     (swap.py:181) and engine µs per iteration (engine.py:351).
 
     which="reference": the unmodified reference, installed offline into
-    baseline/_ref; if absent there, says so.  which="ours": this package."""
+    baseline/_ref; if absent there, says so.  which="ours": this package's
+    Python control plane; which="native": its C++ control plane
+    (native_ctrl.py, libkvctrl)."""
     t = TRACES["stress_markov"]
     doc = {"ablation": "full", "block": {"bytes_per_block": 2097152},
            "gpu_pool": {"total_blocks": 512}, "cpu_pool": {"total_blocks": t["cpu"]},
@@ -292,8 +300,10 @@ def control_plane_cost(which: str) -> dict:
         from paper_2411_18424_b200.engine import Engine as E
         from paper_2411_18424_b200.workload import generate
         cfg, wl, _ = mconfig.build(doc)
-        eng = E(cfg, generate(wl))
-        label = "paper_2411_18424_b200 (this package, replay mode)"
+        cp = "native" if which == "native" else "python"
+        eng = E(cfg, generate(wl), control_plane=cp)
+        label = ("paper_2411_18424_b200 (this package, replay mode, "
+                 + ("native C++ control plane)" if cp == "native" else "Python control plane)"))
     hooks = {"plan_swap_out": (eng.store, "plan_swap_out"),
              "plan_swap_in": (eng.store, "plan_swap_in"),
              "allocate": (eng.pool, "allocate"), "dispatch": (eng.manager, "dispatch")}
@@ -497,7 +507,8 @@ def run_ours(args, geo):
     # the same leg with the kernel carrying both directions (TMA bulk), and
     # under the serving policy (LSU, op flags, pace + budget)
     e2e_kernel = run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, "throughput")
-    e2e_serving = run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, "latency")
+    e2e_serving = run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world,
+                          args.serving_policy)
     dp.set_launch("out", args.ctas, 0)
     dp.set_launch("in", args.ctas, 0)
 
@@ -524,18 +535,22 @@ def run_ours(args, geo):
             print(f"bench: SM partition unavailable ({exc}); sharing all SMs", file=sys.stderr)
             args.sm_partition = 0
 
-    # ---- serving configuration: paced swaps under a concurrent decode load ----
+    # ---- serving configuration: swaps under a concurrent decode load ----
     serving = None
     if rank == 0:
-        serving = {"full_rate_shared_sms": serving_interference(dp, dev, s, 0, "latency")}
+        g = not args.stream_decode
+        serving = {"full_rate_shared_sms": serving_interference(dp, dev, s, 0, "latency",
+                                                                  graph=g)}
         if args.sm_partition:
             part = f"swap_on_{args.sm_partition}_sms"
-            serving["full_rate_" + part] = serving_interference(dp, dev, s, args.sm_partition,
-                                                                "latency")
-            serving["in_share_" + part] = serving_interference(dp, dev, s, args.sm_partition,
-                                                               "latency_share")
             serving[args.serving_policy + "_" + part] = serving_interference(
-                dp, dev, s, args.sm_partition, args.serving_policy)
+                dp, dev, s, args.sm_partition, args.serving_policy, graph=g)
+            # the same policy with the decode kernels launched one by one: their
+            # command fetches share the PCIe link with the swap-in
+            serving[args.serving_policy + "_stream_decode_" + part] = serving_interference(
+                dp, dev, s, args.sm_partition, args.serving_policy, graph=False)
+            serving["serving_paced_stream_decode_" + part] = serving_interference(
+                dp, dev, s, args.sm_partition, "serving_paced", graph=False)
 
     # ---- live multi-turn preemption traces: P99 TTFT / TBT (metric part 2) ----
     trace = None
@@ -566,7 +581,8 @@ def run_ours(args, geo):
         cpu = {"value": round(rate, 3), "unit": "GB/s", "kind": "port", "sample": sample,
                **host_cpu_info(threads),
                "control_plane": control_plane_cost("reference"),
-               "control_plane_ours": control_plane_cost("ours")}
+               "control_plane_ours": control_plane_cost("ours"),
+               "control_plane_native": control_plane_cost("native")}
     if rank == 0:
         dominant, dom_ms = ("in", in_ms) if sum(in_ms) >= sum(out_ms) else ("out", out_ms)
         achieved = nbytes_dir / (statistics.mean(dom_ms) * 1e-3) / 1e9
@@ -751,7 +767,9 @@ def run_trace(args, geo, dev, name):
                        f"KV reads of every resident token + {decode.bytes_per_us / 1e3:.0f} GB/s "
                        f"weight streaming per rank; FastSwitch swaps under the "
                        f"'{args.serving_policy}' policy",
-           "pattern": t["pattern"], "tp": world, "sm_partition": sms, "runs": {}}
+           "pattern": t["pattern"], "tp": world, "sm_partition": sms,
+           "control_plane": args.control_plane,
+           "decode_launch": "stream" if args.stream_decode else "cuda_graph", "runs": {}}
     for run, mode, impl in (("fastswitch", "full", "kernel"),
                             ("vllm_like", "baseline", "ce_per_block")):
         cfg, wl, _ = mconfig.build({**doc, "ablation": mode})
@@ -761,7 +779,8 @@ def run_trace(args, geo, dev, name):
                      copy_impl=impl, timing=True, sm_partition=args.sm_partition,
                      layered_swap_in=layered,
                      duplex_policy=args.serving_policy if impl == "kernel" else "latency")
-        eng = LiveEngine(cfg, generate(wl), rt, decode, agreement=agreement, layered=layered)
+        eng = LiveEngine(cfg, generate(wl), rt, decode, agreement=agreement, layered=layered,
+                         control_plane=args.control_plane, graph_decode=not args.stream_decode)
         eng.turn_trace = []
         rep = eng.run()
         lat = eng.latency_summary()

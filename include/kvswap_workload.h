@@ -64,7 +64,9 @@ int kvs_stream_read_ex(int device, uint64_t stream, const void* buf, size_t buf_
  * (cudaGraphExecUpdate, *how = 1) or instantiates it (*how = 2) when the
  * step's structure changed; kvs_graph_launch runs it on `stream`.
  * kvs_graph_elapsed reads the time between two marks after the launch
- * completed. */
+ * completed.  A captured kvs_wait_flag parks its hardware queue until the
+ * flag is published: queue the flag's producer (the swap) before launching
+ * the step that waits for it, as the live engine does. */
 typedef struct KvsGraph KvsGraph;
 int kvs_graph_create(int device, int n_marks, KvsGraph** out);
 int kvs_graph_destroy(KvsGraph* g);

@@ -343,9 +343,13 @@ struct KvcPool {
     });
     return found;
   }
-  int64_t reclaimable(int64_t exclude) {
+  int64_t reclaimable(int64_t exclude) {  // sum over victims(): no order needed
     int64_t t = 0;
-    for (Group* g : victims(exclude)) t += g->unused_tail();
+    for (auto& kv : active) {
+      if (exclude != KVC_NONE && kv.first == exclude) continue;
+      const int64_t tail = at(kv.second).unused_tail();
+      if (tail > 0) t += tail;
+    }
     return t;
   }
   int64_t rank_of(int64_t owner) {
@@ -374,7 +378,10 @@ struct KvcPool {
   void allocate(int64_t req, int64_t want, int64_t expected, bool reclaim,
                 std::vector<Group>& grants, std::vector<std::pair<int64_t, int64_t>>& carved) {
     if (want < 1) fail(KVC_ERR_VALUE, "want_blocks must be >= 1, got " + i2s(want));
-    const int64_t supply = free_total + (reclaim ? reclaimable(req) : 0);
+    // Carvable tails only matter when the free blocks fall short (the
+    // reference sums them on every call, alloc.py:224-229; same decision).
+    int64_t supply = free_total;
+    if (reclaim && supply < want) supply += reclaimable(req);
     if (supply < want)
       fail(KVC_ERR_OOM, "need " + i2s(want) + " blocks, supply " + i2s(supply) + " (free " +
                             i2s(free_total) + ")");

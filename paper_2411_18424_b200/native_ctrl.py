@@ -68,9 +68,27 @@ def cabi_backend():
     return kvctrl_cabi
 
 
+_new = object.__new__
+
+
 def _group(t) -> BlockGroup:
-    return BlockGroup(id=t[0], start=t[1], length=t[2], free=t[3], owner=t[4], active=t[5],
+    g = _new(BlockGroup)  # field-for-field BlockGroup without the dataclass __init__
+    g.__dict__.update(id=t[0], start=t[1], length=t[2], free=t[3], owner=t[4], active=t[5],
                       filled=t[6])
+    return g
+
+
+def _used(gid: int, start: int, length: int, owner: int, active: bool) -> BlockGroup:
+    g = _new(BlockGroup)
+    g.__dict__.update(id=gid, start=start, length=length, free=False, owner=owner,
+                      active=active, filled=0)
+    return g
+
+
+def _op(t) -> TransferOp:
+    o = _new(TransferOp)  # frozen dataclass: fill its fields without __setattr__
+    o.__dict__.update(blocks=t[0], gpu_start=t[1], cpu_start=t[2])
+    return o
 
 
 # ---------------------------------------------------------------------------
@@ -131,8 +149,7 @@ class NativeBlockGroupPool:
                  reclaim: bool = True) -> AllocResult:
         grants, carved = self._b.pool_allocate(self._h, req, want_blocks, expected_total,
                                                reclaim)
-        groups = [BlockGroup(id=g, start=s, length=n, free=False, owner=req)
-                  for g, s, n in grants]
+        groups = [_used(g, s, n, req, False) for g, s, n in grants]
         groups[-1].active = True
         return AllocResult(groups=groups, reclaimed_from=carved)
 
@@ -422,8 +439,8 @@ class NativeCpuStore:
     @staticmethod
     def _plan(req: int, direction: str, t) -> SwapPlan:
         moved, reused, ops, refresh = t
-        return SwapPlan(req, direction, [TransferOp(*o) for o in ops], moved, reused,
-                        [TransferOp(*o) for o in refresh])
+        return SwapPlan(req, direction, [_op(o) for o in ops], moved, reused,
+                        [_op(o) for o in refresh] if refresh else [])
 
     def plan_swap_out(self, req: int, gpu_footprint: int, gpu_extents: list[tuple[int, int]],
                       tokens: Optional[int] = None) -> SwapPlan:

@@ -224,12 +224,19 @@ DUPLEX_POLICIES = {
                          "priority": "in"},
     "latency_share": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
                       "share": {"in": 42.0}},
-    # serving: paced below the link in both directions.  A decode step made
-    # of per-layer kernels pays ~0.2-0.4% per GB/s of concurrent swap-in HBM
-    # writes (profiles/r02_interference_layers.json); on the live trace swap-in
-    # 40 / swap-out 20 GB/s holds the stall under 10% with the same TTFT tail
-    # as full rate (profiles/r02_live_policy_probe.json).
-    "serving": {"out": (8, 512, 20.0), "in": (8, 256, 40.0), "budget": 60.0},
+    # serving: the link rate in each direction (swap-in bounded by reads in
+    # flight, swap-out paced at 52 GB/s), with 42 GB/s of a 60 GB/s budget
+    # reserved for swap-in while both run.  With the decode step launched as
+    # a CUDA graph (live.DecodeGraph) a full-rate swap-in costs a 32-layer
+    # step +9% in the worst case and +7% on the live trace
+    # (profiles/r02_graph_decode.json).
+    "serving": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
+                "share": {"in": 42.0}},
+    # serving_paced: for decode kernels launched one by one on a stream, whose
+    # command fetches queue behind a saturating swap-in's PCIe reads: paced
+    # below the link (in 40 / out 20 GB/s) the stall stays under 10%
+    # (profiles/r02_live_policy_probe.json).
+    "serving_paced": {"out": (8, 512, 20.0), "in": (8, 256, 40.0), "budget": 60.0},
     # the serving policy on the TMA bulk kernels (op / plane flags from the
     # elected thread's store side): same pace and budget, fewer SM threads
     "latency_bulk": {"out": (8, 0, 52.0), "in": (8, 0, 0.0), "budget": 60.0, "path": "bulk"},

@@ -65,10 +65,14 @@ def test_graph_updates_in_place_and_runs_each_iterations_parameters(cuda_ok):
 
 
 def test_plane_flag_waits_are_graph_nodes(cuda_ok):
+    """The producer of the flag is queued first (as in the live engine, where
+    the swap-in is dispatched before the step that waits for its planes): a
+    stream wait parks its hardware queue, so a producer queued after it on a
+    queue it shares could never run."""
     cache, host, dp = _setup()
     flags = torch.zeros(4, dtype=torch.int32, device="cuda:0")
     g = DecodeGraph("cuda:0", marks=2)
-    comp = torch.cuda.Stream()
+    comp, side = torch.cuda.Stream(), torch.cuda.Stream()
     segs = np.array([[1, 0, 16, 9]], dtype=np.int64)
     st = g.begin()
     dp.wait_flag(st, flags.data_ptr() + 4 * 2, 5)  # waits for flags[2] >= 5
@@ -78,14 +82,17 @@ def test_plane_flag_waits_are_graph_nodes(cuda_ok):
     g.end()
     cache.planes.zero_()
     torch.cuda.synchronize()
-    g.launch(comp)
-    time.sleep(0.05)
-    assert not comp.query()  # parked on the flag
-    assert int(cache.planes.view(torch.int32).abs().sum().item()) == 0
-    side = torch.cuda.Stream()
     with torch.cuda.stream(side):
-        flags[2] = 5
-    comp.synchronize()
+        torch.cuda._sleep(300_000_000)  # ~0.15 s of GPU cycles, then publish the flag
+        flags[2:3].fill_(5)
+    g.launch(comp)
+    early = comp.query()
+    deadline = time.time() + 20
+    while not comp.query():
+        assert time.time() < deadline, "the graph never left its flag wait"
+        time.sleep(0.002)
+    assert not early  # it was parked on the flag
+    torch.cuda.synchronize()
     assert int(cache.planes.view(torch.int32).abs().sum().item()) > 0
     assert g.elapsed(0, 1) > 0
     g.close()

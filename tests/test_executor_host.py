@@ -51,7 +51,12 @@ def test_duplex_policies_are_well_formed():
     lat = DUPLEX_POLICIES["latency"]
     assert 0 < lat["out"][2] < 63.0
     assert lat["in"][2] == 0.0 and lat["in"][0] * lat["in"][1] // 32 * 4096 <= 512 * 1024
-    # the live traces' policy: both directions paced below the link, under the budget
+    # the live traces' policy (graph-launched decode): the link rate each way,
+    # swap-in keeps a reserved share of the shared budget while both run
     srv = DUPLEX_POLICIES["serving"]
-    assert 0 < srv["out"][2] <= srv["in"][2] < 63.0
-    assert srv["out"][2] + srv["in"][2] <= srv["budget"]
+    assert srv["in"][2] == 0.0 and 0 < srv["out"][2] < 63.0
+    assert 0 < srv["share"]["in"] < srv["budget"]
+    # stream-launched decode: both directions paced below the link, under the budget
+    sp = DUPLEX_POLICIES["serving_paced"]
+    assert 0 < sp["out"][2] <= sp["in"][2] < 63.0
+    assert sp["out"][2] + sp["in"][2] <= sp["budget"]

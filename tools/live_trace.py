@@ -96,7 +96,7 @@ def main():
     ap.add_argument("--modes", default="full:kernel,baseline:ce_per_block")
     ap.add_argument("--weights-gib", type=int, default=16)
     ap.add_argument("--verify", action="store_true")
-    ap.add_argument("--policy", default="latency")
+    ap.add_argument("--policy", default="serving")
     ap.add_argument("--sm-partition", type=int, default=0,
                     help="swap kernels on their own N-SM green context, decode on the rest")
     ap.add_argument("--layered", action="store_true",
