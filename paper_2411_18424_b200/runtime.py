@@ -218,7 +218,7 @@ class Runtime:
         segs = self.segments(engine, [(req, 0, valid)])
         with torch.cuda.stream(self.executor.compute):
             self._mismatch.zero_()
-        self.dataplane.kv_tokens(1, segs, stream=stream or self.executor.compute,
+        self.dataplane.kv_tokens(1, segs, stream=self.executor.compute,
                                  mismatch_ptr=self._mismatch.data_ptr())
         self.executor.compute.synchronize()
         bad = int(self._mismatch.item())
