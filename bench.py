@@ -93,7 +93,7 @@ def parse(argv=None):
     ap.add_argument("--sm-partition", type=int, default=8,
                     help="serving + trace: swap kernels on their own N-SM green context, "
                          "decode on the rest (0 = share all SMs)")
-    ap.add_argument("--e2e-policy", default="throughput_mix",
+    ap.add_argument("--e2e-policy", default="throughput_staged",
                     help="StreamExecutor duplex policy of the headline e2e leg")
     ap.add_argument("--serving-policy", default="serving",
                     help="StreamExecutor duplex policy of the live traces' FastSwitch arm")
@@ -502,6 +502,34 @@ def run_ours(args, geo):
     out_gbs = nbytes_dir / (statistics.mean(out_ms) * 1e-3) / 1e9
     in_gbs = nbytes_dir / (statistics.mean(in_ms) * 1e-3) / 1e9
 
+    # ---- the same steps on the staged copy-engine path (whole host runs on
+    #      the copy engines through an HBM ring + gather / scatter kernels) ----
+    def step_staged(evs):
+        evs[0].record(s)
+        dp.baseline("out", 2, out_ops, stream=s)
+        evs[1].record(s)
+        dp.baseline("in", 2, in_ops, stream=s)
+        evs[2].record(s)
+
+    sev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)]
+           for _ in range(args.warmup + args.steps)]
+    for k in range(args.warmup + args.steps):
+        step_staged(sev[k])
+    torch.cuda.synchronize()
+    sev = sev[args.warmup:]
+    st_out = [e[0].elapsed_time(e[1]) for e in sev]
+    st_in = [e[1].elapsed_time(e[2]) for e in sev]
+    staged = {
+        "engine": "copy engines, one copy per host run (<= 64 MiB slot) + kvs_stage_kernel "
+                  "gather / scatter (HBM ring, 4 slots)",
+        "per_direction_gbs": {"out": round(nbytes_dir / (statistics.mean(st_out) * 1e-3) / 1e9, 3),
+                              "in": round(nbytes_dir / (statistics.mean(st_in) * 1e-3) / 1e9, 3)},
+        "gbs": round(2 * nbytes_dir * len(sev) / ((sum(st_out) + sum(st_in)) * 1e-3) / 1e9, 3),
+        "frac": None,
+    }
+    staged["frac"] = {d: round(v / PCIE_GEN5_X16_GBS, 4)
+                      for d, v in staged["per_direction_gbs"].items()}
+
     # ---- e2e: public API (control plane + dispatch) with host round trip ----
     e2e = run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, args.e2e_policy)
     # the same leg with the kernel carrying both directions (TMA bulk), and
@@ -600,6 +628,9 @@ def run_ours(args, geo):
             "host_pool": {"blocks": host_pool, "numa_node": host_numa,
                           "numa_node_per_rank": numa_per_rank, "numa_nodes": numa_nodes()},
             "per_direction_gbs": {"out": round(out_gbs, 3), "in": round(in_gbs, 3)},
+            # every timed step's per-direction time: a dip here is the box, not a mean
+            "step_ms": {"out": [round(x, 2) for x in out_ms], "in": [round(x, 2) for x in in_ms]},
+            "staged": staged,
             "roofline": {"bound": "pcie", "achieved": round(achieved, 3),
                          "peak": PCIE_GEN5_X16_GBS, "unit": "GB/s",
                          "frac": round(achieved / PCIE_GEN5_X16_GBS, 4), "traffic": traffic,
@@ -688,12 +719,12 @@ def run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, policy):
         step()
     barrier()
     torch.cuda.synchronize()
-    l0 = ex.launches
+    l0 = dp.launches  # every libkvswap kernel: swap kernels and staged gather / scatter
     t0 = time.perf_counter()
     for _ in range(args.steps):
         step()
     el = max_over_ranks(time.perf_counter() - t0)
-    launches = ex.launches - l0
+    launches = dp.launches - l0
 
     blocks = torch.as_tensor(np.concatenate([np.arange(g, g + b) for t in tables for g, b in t]),
                              device=dev)
@@ -940,14 +971,15 @@ def ce_peak(dev, host, cache):
     return res
 
 
-SWEEP_ENGINES = ("kernel_lsu", "kernel_bulk", "ce_per_block", "ce_per_run", "ce_batch")
+SWEEP_ENGINES = ("kernel_lsu", "kernel_bulk", "ce_per_block", "ce_per_run", "ce_staged")
 
 
 def group_sweep(dp, s, s2):
     """Config 2: swap GB/s vs group size for every engine —
     K1/K2 LSU (v1) and TMA bulk (v2), K3 per-block (vLLM swap_blocks, the
     reference's split_single path, swap.py:170-179), K3 per-run (one 2D copy
-    per run), K4 cudaMemcpyBatchAsync — per direction (a 4096-block plan) and
+    per run), staged (whole host runs on the copy engines through an HBM ring
+    + a gather / scatter kernel) — per direction (a 4096-block plan) and
     both directions at once (2048-block plans each way on disjoint halves of
     the pools; combined GB/s over the union of both streams' lifetimes)."""
     import torch
@@ -964,7 +996,7 @@ def group_sweep(dp, s, s2):
             dp.set_path(d, "bulk" if engine == "kernel_bulk" else "lsu")
             dp.swap(d, ops, stream=stream)
         else:
-            dp.baseline(d, ("ce_per_block", "ce_per_run", "ce_batch").index(engine), ops,
+            dp.baseline(d, ("ce_per_block", "ce_per_run", "ce_staged").index(engine), ops,
                         stream=stream)
 
     def timed(fn_by_stream):

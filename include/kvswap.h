@@ -55,7 +55,9 @@ extern "C" {
 /* kvs_memcpy_baseline modes (copy-engine comparators). */
 #define KVS_BASE_PER_BLOCK 0 /* vLLM: one cudaMemcpyAsync per (plane, block)      */
 #define KVS_BASE_PER_RUN 1   /* block groups on the CE: one cudaMemcpy2DAsync per (plane, op) */
-#define KVS_BASE_BATCH 2     /* one cudaMemcpyBatchAsync per plan (CUDA >= 12.8)  */
+#define KVS_BASE_STAGED 2    /* staged: one large contiguous host copy per slot of
+                                a 64 MiB HBM staging ring + a device gather/scatter
+                                kernel between the ring and the planes            */
 
 /* Kernel paths (kvs_set_path). */
 #define KVS_PATH_LSU 0  /* v1: warps move 16-B vectors with LDG/STG (default)       */
@@ -221,11 +223,32 @@ int kvs_wait_flag(uint64_t stream, const uint32_t* flag, uint32_t value);
 /* Number of kernels this handle has launched (gpu_launches evidence). */
 int64_t kvs_launch_count(const KvsHandle* h);
 
-/* Copy-engine comparators for the same plan (vLLM per-block, per-run 2D,
- * cudaMemcpyBatchAsync).  Reference: split_single (swap.py:170-179) is the
- * per-block mode; block groups (alloc.py) are the per-run mode. */
+/* Copy-engine paths for the same plan: vLLM per-block, per-run 2D, and
+ * staged.  Reference: split_single (swap.py:170-179) is the per-block mode;
+ * block groups (alloc.py) are the per-run mode.
+ *
+ * KVS_BASE_STAGED is a product path, not only a comparator.  SM- and
+ * TMA-issued host traffic leaves in 128 B PCIe TLPs, which caps the kernels
+ * near 53 GB/s.  The copy engines use larger TLPs.  But a host block image is
+ * [plane][chunk] while HBM holds one plane per layer, so a direct copy is
+ * chunk-sized.  The staged mode therefore splits the work:
+ *   - the copy engine moves each run of adjacent host blocks as ONE
+ *     contiguous copy (up to a slot, 64 MiB) between the host pool and a
+ *     ring of HBM staging slots, on `stream`;
+ *   - a gather (out) / scatter (in) kernel moves the slot's blocks between
+ *     the ring and the planes at HBM speed, on a per-direction auxiliary
+ *     stream of the handle, joined to `stream` with events.
+ * Completion is stream-ordered: work queued on `stream` after the call sees
+ * every byte.  The ring is allocated on first use (kvs_set_staging).  One
+ * stream per direction per handle, as for kvs_swap. */
 int kvs_memcpy_baseline(KvsHandle* h, int dir, int mode, const int32_t* ops,
                         int32_t n_ops, uint64_t stream);
+
+/* Staging ring of KVS_BASE_STAGED, per direction: `slots` (2..16) slots of
+ * `slot_bytes` (rounded down to whole blocks, at least one block).  0 keeps
+ * the default (4 x 64 MiB).  Frees the current ring (synchronising with its
+ * users) so the next staged call reallocates it. */
+int kvs_set_staging(KvsHandle* h, int64_t slot_bytes, int slots);
 
 /* Spatial SM partition for the swap kernels (green contexts): the swap side
  * gets a group of >= swap_sms SMs (rounded up to the architecture's

@@ -59,6 +59,7 @@ EXPORTED_SYMBOLS = (
     "kvs_wait_flag",
     "kvs_launch_count",
     "kvs_memcpy_baseline",
+    "kvs_set_staging",
     "kvs_host_alloc",
     "kvs_host_free",
     "kvs_sm_partition",
@@ -156,6 +157,8 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_memcpy_baseline.argtypes = [
         c.c_void_p, c.c_int, c.c_int, c.c_void_p, c.c_int32, c.c_uint64,
     ]
+    lib.kvs_set_staging.restype = c.c_int
+    lib.kvs_set_staging.argtypes = [c.c_void_p, c.c_int64, c.c_int]
     lib.kvs_host_alloc.restype = c.c_int
     lib.kvs_host_alloc.argtypes = [
         c.c_size_t, c.c_int, c.c_int, c.POINTER(c.c_void_p), c.POINTER(c.c_void_p),

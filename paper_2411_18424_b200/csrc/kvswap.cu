@@ -574,6 +574,16 @@ struct KvsHandle {
   int layer_group = 0;           // layered order: planes per group (0 = auto)
   unsigned long long* d_bucket = nullptr;
   int64_t launches = 0;
+  // KVS_BASE_STAGED: per-direction HBM staging ring, auxiliary stream, events.
+  int64_t stage_cfg_bytes = 0;  // requested slot bytes (0 = default)
+  int stage_cfg_slots = 0;      // requested slots (0 = default)
+  char* d_stage[2] = {nullptr, nullptr};
+  int64_t stage_slot_blocks[2] = {0, 0};
+  int stage_slots[2] = {0, 0};
+  uint64_t stage_next[2] = {0, 0};  // ring cursor
+  cudaStream_t stage_aux[2] = {nullptr, nullptr};
+  cudaEvent_t stage_start[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> stage_filled[2], stage_free[2];
 };
 
 namespace {
@@ -748,6 +758,199 @@ struct HostAlloc {
 std::mutex g_host_mu;
 std::unordered_map<void*, HostAlloc> g_host_allocs;
 
+// ---------------------------------------------------------------------------
+// Staged copy-engine path (KVS_BASE_STAGED, include/kvswap.h).
+// SM- and TMA-issued host traffic leaves in 128 B TLPs (~53 GB/s payload
+// ceiling on Gen5 x16); the copy engines' larger TLPs reach ~55-57 GB/s, but
+// only on long contiguous copies, and a run of host block images is
+// contiguous only as [block][plane][chunk].  So the copy engine moves whole
+// host runs into / out of an HBM staging slot, and this kernel does the
+// layout change between the slot ([j][plane][chunk]) and the planes at HBM
+// speed (a 64 MiB slot is ~20 us of HBM time against ~1.2 ms on the link).
+// ---------------------------------------------------------------------------
+constexpr int kStageMapMax = 1024;  // blocks per slot (kernel parameter table)
+constexpr int64_t kDefaultStageBytes = 64ll << 20;
+constexpr int kDefaultStageSlots = 4;
+
+struct StageParams {
+  const uint64_t* planes;  // device array [num_planes] of plane bases
+  char* slot;
+  int64_t chunk;
+  int64_t stride;
+  uint32_t num_planes;
+  uint32_t n_blocks;
+  int32_t gpu_block[kStageMapMax];  // GPU block of slot block j
+};
+
+// DIR == KVS_DIR_OUT: planes -> slot (gather).  DIR == KVS_DIR_IN: slot -> planes.
+template <int DIR>
+__global__ void __launch_bounds__(512) kvs_stage_kernel(const __grid_constant__ StageParams p) {
+  const uint32_t units = p.n_blocks * p.num_planes;  // (j, plane) chunks, slot order
+  const int64_t vecs = p.chunk / kVecBytes;
+  for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const uint32_t j = u / p.num_planes;
+    const uint32_t pl = u - j * p.num_planes;
+    int4* slot = reinterpret_cast<int4*>(p.slot + static_cast<int64_t>(u) * p.chunk);
+    int4* gpu = reinterpret_cast<int4*>(reinterpret_cast<char*>(__ldg(p.planes + pl)) +
+                                        static_cast<int64_t>(p.gpu_block[j]) * p.stride);
+    const int4* src = DIR == KVS_DIR_OUT ? gpu : slot;
+    int4* dst = DIR == KVS_DIR_OUT ? slot : gpu;
+    int64_t v = threadIdx.x;
+    for (; v + 3 * blockDim.x < vecs; v += 4 * blockDim.x) {
+      int4 a = src[v], b = src[v + blockDim.x], c = src[v + 2 * blockDim.x],
+           d = src[v + 3 * blockDim.x];
+      dst[v] = a;
+      dst[v + blockDim.x] = b;
+      dst[v + 2 * blockDim.x] = c;
+      dst[v + 3 * blockDim.x] = d;
+    }
+    for (; v < vecs; v += blockDim.x) dst[v] = src[v];
+  }
+}
+
+void stage_release(KvsHandle* h, int dir) {
+  if (h->stage_aux[dir]) cudaStreamSynchronize(h->stage_aux[dir]);
+  if (h->d_stage[dir]) cudaFree(h->d_stage[dir]);
+  for (cudaEvent_t e : h->stage_filled[dir]) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->stage_free[dir]) cudaEventDestroy(e);
+  if (h->stage_start[dir]) cudaEventDestroy(h->stage_start[dir]);
+  if (h->stage_aux[dir]) cudaStreamDestroy(h->stage_aux[dir]);
+  h->d_stage[dir] = nullptr;
+  h->stage_filled[dir].clear();
+  h->stage_free[dir].clear();
+  h->stage_start[dir] = nullptr;
+  h->stage_aux[dir] = nullptr;
+  h->stage_slot_blocks[dir] = 0;
+  h->stage_slots[dir] = 0;
+}
+
+int stage_ensure(KvsHandle* h, int dir) {
+  if (h->d_stage[dir] != nullptr) return KVS_OK;
+  const int64_t hblk = h->geo.plane_chunk_bytes * h->geo.num_planes;
+  const int64_t want = h->stage_cfg_bytes > 0 ? h->stage_cfg_bytes : kDefaultStageBytes;
+  int64_t blocks = want / hblk;
+  if (blocks < 1) blocks = 1;
+  if (blocks > kStageMapMax) blocks = kStageMapMax;
+  if (static_cast<uint64_t>(blocks) * h->geo.num_planes > 0xFFFFFFFFull) return KVS_ERR_RANGE;
+  const int slots = h->stage_cfg_slots > 0 ? h->stage_cfg_slots : kDefaultStageSlots;
+  int lo = 0, hi = 0;
+  int rc = cuda_rc(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  // Highest priority: a slot's gather / scatter is short and gates the link.
+  if (!rc) rc = cuda_rc(cudaStreamCreateWithPriority(&h->stage_aux[dir], cudaStreamNonBlocking, hi));
+  if (!rc) rc = cuda_rc(cudaMalloc(&h->d_stage[dir], static_cast<size_t>(slots) * blocks * hblk));
+  if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&h->stage_start[dir], cudaEventDisableTiming));
+  for (int q = 0; q < slots && !rc; ++q) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    rc = cuda_rc(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+    if (!rc) h->stage_filled[dir].push_back(a);
+    if (!rc) rc = cuda_rc(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+    if (!rc) h->stage_free[dir].push_back(b);
+  }
+  if (rc) {
+    cudaGetLastError();
+    stage_release(h, dir);
+    return rc;
+  }
+  h->stage_slot_blocks[dir] = blocks;
+  h->stage_slots[dir] = slots;
+  return KVS_OK;
+}
+
+// One plan through the staging ring; ops already validated.
+int staged_copy(KvsHandle* h, int dir, const int32_t* ops, int32_t n_ops, cudaStream_t s) {
+  int rc = stage_ensure(h, dir);
+  if (rc) return rc;
+  const int64_t hblk = h->geo.plane_chunk_bytes * h->geo.num_planes;
+  const int64_t cap = h->stage_slot_blocks[dir];
+  const int K = h->stage_slots[dir];
+  cudaStream_t aux = h->stage_aux[dir];
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+  StageParams sp;
+  sp.planes = h->d_planes;
+  sp.chunk = h->geo.plane_chunk_bytes;
+  sp.stride = h->geo.plane_block_stride;
+  sp.num_planes = static_cast<uint32_t>(h->geo.num_planes);
+  if (dir == KVS_DIR_OUT) {
+    // The gather reads KV that work queued on `s` before this call produced.
+    rc = cuda_rc(cudaEventRecord(h->stage_start[dir], s));
+    if (!rc) rc = cuda_rc(cudaStreamWaitEvent(aux, h->stage_start[dir], 0));
+    if (rc) return rc;
+  }
+  std::vector<std::pair<int64_t, int64_t>> segs;  // (cpu_start, blocks): contiguous host runs
+  int32_t n = 0;
+  int last_q = -1;
+  auto flush = [&]() -> int {
+    if (n == 0) return KVS_OK;
+    const int q = static_cast<int>(h->stage_next[dir]++ % static_cast<uint64_t>(K));
+    char* slot = h->d_stage[dir] + static_cast<int64_t>(q) * cap * hblk;
+    sp.slot = slot;
+    sp.n_blocks = static_cast<uint32_t>(n);
+    const uint32_t units = sp.n_blocks * sp.num_planes;
+    const unsigned grid = units < static_cast<uint32_t>(2 * sms) ? units : 2 * sms;
+    int r = KVS_OK;
+    if (dir == KVS_DIR_IN) {
+      // slot q is free once its previous scatter finished
+      r = cuda_rc(cudaStreamWaitEvent(s, h->stage_free[dir][q], 0));
+      int64_t off = 0;
+      for (const auto& sg : segs) {
+        if (r) break;
+        r = cuda_rc(cudaMemcpyAsync(slot + off * hblk, h->host + sg.first * hblk, sg.second * hblk,
+                                    cudaMemcpyHostToDevice, s));
+        off += sg.second;
+      }
+      if (!r) r = cuda_rc(cudaEventRecord(h->stage_filled[dir][q], s));
+      if (!r) r = cuda_rc(cudaStreamWaitEvent(aux, h->stage_filled[dir][q], 0));
+      if (!r) {
+        kvs_stage_kernel<KVS_DIR_IN><<<grid, 512, 0, aux>>>(sp);
+        r = cuda_rc(cudaGetLastError());
+      }
+      if (!r) r = cuda_rc(cudaEventRecord(h->stage_free[dir][q], aux));
+    } else {
+      // slot q is free once the copy that last drained it finished
+      r = cuda_rc(cudaStreamWaitEvent(aux, h->stage_free[dir][q], 0));
+      if (!r) {
+        kvs_stage_kernel<KVS_DIR_OUT><<<grid, 512, 0, aux>>>(sp);
+        r = cuda_rc(cudaGetLastError());
+      }
+      if (!r) r = cuda_rc(cudaEventRecord(h->stage_filled[dir][q], aux));
+      if (!r) r = cuda_rc(cudaStreamWaitEvent(s, h->stage_filled[dir][q], 0));
+      int64_t off = 0;
+      for (const auto& sg : segs) {
+        if (r) break;
+        r = cuda_rc(cudaMemcpyAsync(h->host + sg.first * hblk, slot + off * hblk, sg.second * hblk,
+                                    cudaMemcpyDeviceToHost, s));
+        off += sg.second;
+      }
+      if (!r) r = cuda_rc(cudaEventRecord(h->stage_free[dir][q], s));
+    }
+    if (!r) h->launches += 1;
+    last_q = q;
+    n = 0;
+    segs.clear();
+    return r;
+  };
+  for (int32_t i = 0; i < n_ops && !rc; ++i) {
+    const int64_t b = ops[3 * i], g0 = ops[3 * i + 1], c0 = ops[3 * i + 2];
+    for (int64_t k = 0; k < b && !rc;) {
+      const int64_t take = (b - k) < (cap - n) ? (b - k) : (cap - n);
+      if (!segs.empty() && segs.back().first + segs.back().second == c0 + k)
+        segs.back().second += take;  // host run continues across ops
+      else
+        segs.emplace_back(c0 + k, take);
+      for (int64_t t = 0; t < take; ++t) sp.gpu_block[n + t] = static_cast<int32_t>(g0 + k + t);
+      n += static_cast<int32_t>(take);
+      k += take;
+      if (n == cap) rc = flush();
+    }
+  }
+  if (!rc) rc = flush();
+  // swap-in: `s` resumes after the last scatter (the aux stream is in order)
+  if (!rc && dir == KVS_DIR_IN && last_q >= 0)
+    rc = cuda_rc(cudaStreamWaitEvent(s, h->stage_free[dir][last_q], 0));
+  return rc;
+}
+
 }  // namespace
 
 extern "C" {
@@ -823,6 +1026,7 @@ int kvs_destroy(KvsHandle* h) {
   if (h->d_plane_ctr) cudaFree(h->d_plane_ctr);
   if (h->d_op_ctr) cudaFree(h->d_op_ctr);
   if (h->d_bucket) cudaFree(h->d_bucket);
+  for (int d = 0; d < 2; ++d) stage_release(h, d);
   delete h;
   return KVS_OK;
 }
@@ -1033,28 +1237,21 @@ int kvs_memcpy_baseline(KvsHandle* h, int dir, int mode, const int32_t* ops, int
       }
     return KVS_OK;
   }
-  if (mode == KVS_BASE_BATCH) {
+  if (mode == KVS_BASE_STAGED) {
     if (blocks == 0) return KVS_OK;
-    const size_t n = static_cast<size_t>(blocks) * P;
-    std::vector<void*> dsts(n), srcs(n);
-    std::vector<size_t> sizes(n, static_cast<size_t>(chunk));
-    size_t k = 0;
-    for (int32_t i = 0; i < n_ops; ++i)
-      for (int32_t b = 0; b < ops[3 * i]; ++b)
-        for (int p = 0; p < P; ++p, ++k) {
-          char* g = gpu_addr(p, ops[3 * i + 1] + b);
-          char* c = host_addr(p, ops[3 * i + 2] + b);
-          dsts[k] = dir == KVS_DIR_OUT ? static_cast<void*>(c) : static_cast<void*>(g);
-          srcs[k] = dir == KVS_DIR_OUT ? static_cast<void*>(g) : static_cast<void*>(c);
-        }
-    cudaMemcpyAttributes attr;
-    std::memset(&attr, 0, sizeof(attr));
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail_idx = 0;
-    return cuda_rc(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), n, &attr,
-                                        &attr_idx, 1, &fail_idx, s));
+    return staged_copy(h, dir, ops, n_ops, s);
   }
   return KVS_ERR_INVALID;
+}
+
+int kvs_set_staging(KvsHandle* h, int64_t slot_bytes, int slots) {
+  if (h == nullptr || slot_bytes < 0 || slots < 0 || slots == 1 || slots > 16)
+    return KVS_ERR_INVALID;
+  cudaSetDevice(h->device);
+  for (int d = 0; d < 2; ++d) stage_release(h, d);
+  h->stage_cfg_bytes = slot_bytes;
+  h->stage_cfg_slots = slots;
+  return KVS_OK;
 }
 
 int kvs_host_alloc(size_t bytes, int numa_node, int flags, void** host, void** dev) {

@@ -331,6 +331,11 @@ class SwapDataPlane:
         _lib.check(self.lib.kvs_set_path(self.handle, _lib.DIRECTIONS[direction],
                                          _lib.PATHS[path], piece_bytes, stages), "kvs_set_path")
 
+    def set_staging(self, slot_bytes: int = 0, slots: int = 0) -> None:
+        """Staging ring of the staged copy-engine path (0 = default 4 x 64 MiB)."""
+        _lib.check(self.lib.kvs_set_staging(self.handle, int(slot_bytes), int(slots)),
+                   "kvs_set_staging")
+
     def set_pace(self, direction: str, gbps: float = 0.0) -> None:
         """Hold one direction's LSU kernel to `gbps` GB/s (0 = unpaced)."""
         _lib.check(self.lib.kvs_set_pace(self.handle, _lib.DIRECTIONS[direction], float(gbps)),
@@ -416,6 +421,9 @@ class SwapDataPlane:
 
     def baseline(self, direction: str, mode: int, ops: OpsLike,
                  stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Copy-engine path for the plan (include/kvswap.h): 0 per block
+        (vLLM swap_blocks), 1 per run (2D), 2 staged (whole host runs through
+        an HBM staging ring + a gather / scatter kernel)."""
         arr = ops_array(ops)
         rc = self.lib.kvs_memcpy_baseline(self.handle, _lib.DIRECTIONS[direction], mode,
                                           arr.ctypes.data_as(ctypes.c_void_p), arr.shape[0],

@@ -185,7 +185,7 @@ class TransferRecord:
         return self.done
 
 
-COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
+COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_staged")
 
 # Launch shape and pacing per direction (profiles/r01_interference_*.json,
 # profiles/r01_duplex_bw.json).  Unpaced, SM stores to host memory are issued
@@ -210,12 +210,13 @@ COPY_IMPLS = ("kernel", "ce_per_block", "ce_per_run", "ce_batch")
 #                preemptions leaves a concurrent resume ~10 GB/s; strict
 #                swap-in priority starves the preemptions instead;
 #   throughput_mix — bulk migration with one engine per direction: swap-out
-#                on the TMA bulk kernel, swap-in on the copy engines (one
-#                batched copy per plan).  SM-issued host traffic in both
-#                directions tops out at 75-80 GB/s combined; the e2e leg
-#                measured bulk out + CE in at 88.3 GB/s vs 78.4 bulk both ways
-#                and 84.8 LSU out + CE in (profiles/r02_e2e_policy_probe.json);
-#                plan-level waits;
+#                on the TMA bulk kernel, swap-in on the copy engines (staged:
+#                whole host runs into an HBM ring, then a scatter kernel).
+#                SM-issued host traffic in both directions tops out at 75-80
+#                GB/s combined, and one engine per direction avoids that cap
+#                (profiles/r02_e2e_policy_probe.json); plan-level waits;
+#   throughput_staged — bulk migration with both directions on the staged
+#                copy-engine path (larger PCIe TLPs than SM-issued traffic);
 #   unpaced    — out 8x512, in 32x512, no pacing (round-1 default shape).
 DUPLEX_POLICIES = {
     "latency": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0},
@@ -243,7 +244,10 @@ DUPLEX_POLICIES = {
     "throughput": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0, "path": "bulk",
                    "signals": "plan"},
     "throughput_mix": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0,
-                       "path": "bulk", "engine": {"in": "ce_batch"}, "signals": "plan"},
+                       "path": "bulk", "engine": {"in": "ce_staged"}, "signals": "plan"},
+    "throughput_staged": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0,
+                          "path": "bulk", "engine": {"out": "ce_staged", "in": "ce_staged"},
+                          "signals": "plan"},
     "unpaced": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0},
 }
 

@@ -39,7 +39,7 @@ def duel():
     return [Conversation(0, [(320, 320)], 0, 0), Conversation(1, [(320, 320)], 1000, 0)]
 
 
-@pytest.mark.parametrize("copy_impl", ["kernel", "ce_per_block", "ce_batch"])
+@pytest.mark.parametrize("copy_impl", ["kernel", "ce_per_block", "ce_staged"])
 def test_duel_bytes_and_golden_decisions(cuda_ok, copy_impl):
     cfg = _cfg_small()
     rt = _runtime(cfg, copy_impl=copy_impl)

@@ -36,7 +36,7 @@ SEEDS = int(os.environ.get("KVS_FUZZ_SEEDS", "1"))  # more for a soak run
 
 @pytest.mark.parametrize("seed", range(SEEDS))
 @pytest.mark.parametrize("mode", ["ops", "layered", "bulk", "bulk_ops", "bulk_layered",
-                                  "partition"])
+                                  "partition", "staged", "mix"])
 def test_random_interleavings_match_program_order(cuda_ok, mode, seed):
     torch = cuda_ok
     from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPlane
@@ -49,12 +49,16 @@ def test_random_interleavings_match_program_order(cuda_ok, mode, seed):
     host = HostKVPool(C, geo.block_bytes)
     dp = SwapDataPlane(cache, host)
     policy = {"bulk": "throughput", "bulk_ops": "latency_bulk",
-              "bulk_layered": "latency_bulk"}.get(mode, "latency")
+              "bulk_layered": "latency_bulk", "staged": "throughput_staged",
+              "mix": "throughput_mix"}.get(mode, "latency")
+    if mode in ("staged", "mix"):
+        dp.set_staging(2 * geo.block_bytes, 2)  # tiny ring: plans span slots, slots recycle
     ex = StreamExecutor(dp, duplex_policy=policy, layered_swap_in=mode.endswith("layered"),
                         sm_partition=8 if mode == "partition" else 0)
-    assert ex.op_granular == (mode != "bulk")
+    assert ex.op_granular == (mode not in ("bulk", "staged", "mix"))
     rng = np.random.default_rng([{"ops": 1, "layered": 2, "bulk": 3, "partition": 4,
-                                  "bulk_ops": 5, "bulk_layered": 6}[mode], seed])
+                                  "bulk_ops": 5, "bulk_layered": 6, "staged": 7,
+                                  "mix": 8}[mode], seed])
     last_in = None
     gpu = np.zeros((geo.num_planes, G, geo.plane_chunk_bytes), np.uint8)
     hostm = np.zeros((C, geo.block_bytes), np.uint8)
@@ -106,5 +110,5 @@ def test_random_interleavings_match_program_order(cuda_ok, mode, seed):
     ex.synchronize()
     np.testing.assert_array_equal(cache.planes.cpu().numpy(), gpu)
     np.testing.assert_array_equal(host.array, hostm)
-    assert ex.launches > 100
+    assert dp.launches > 100  # swap kernels, or the staged path's gather / scatter kernels
     host.close()

@@ -44,7 +44,7 @@ def test_duplex_policies_are_well_formed():
         assert pol["budget"] >= 0.0
         for d, eng in pol.get("engine", {}).items():
             assert d in ("out", "in") and eng in ("kernel", "ce_per_block", "ce_per_run",
-                                                  "ce_batch"), name
+                                                  "ce_staged"), name
         for d, gbps in pol.get("share", {}).items():
             assert d in ("out", "in") and 0.0 < gbps <= pol["budget"], name
     # serving: swap-out paced below the link, swap-in bounded by reads in flight

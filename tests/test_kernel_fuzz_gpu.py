@@ -2,7 +2,8 @@
 random geometries (1-7 planes, chunks from 16 B to 80 KiB, ragged against
 the 4 KiB piece), random fragmented plans (1-2600 ops: multi-launch), both
 directions, LSU and TMA-bulk paths, plain / op-flagged / layered (random
-plane groups) / signaled launches, random launch shapes."""
+plane groups) / signaled launches, random launch shapes, and the staged
+copy-engine path with random staging rings."""
 
 import os
 
@@ -48,11 +49,15 @@ def test_kernel_entry_points_match_oracle(cuda_ok, case):
     ops = orc.table_to_ops(gpu_tab, cpu_tab)
     flags = torch.zeros(len(ops) + planes + 1, dtype=torch.int32, device="cuda:0")
     fp = flags.data_ptr()
-    kind = str(rng.choice(["plain", "ops", "layered", "signaled"]))
+    kind = str(rng.choice(["plain", "ops", "layered", "signaled", "staged"]))
+    if kind == "staged":  # random ring: 1..40 blocks per slot, 2..5 slots
+        dp.set_staging(int(rng.integers(1, 41)) * geo.block_bytes, int(rng.integers(2, 6)))
 
     def run(direction, seq):
         if kind == "plain":
             dp.swap(direction, ops)
+        elif kind == "staged":
+            dp.baseline(direction, 2, ops)
         elif kind == "ops":
             dp.swap_ops(direction, ops, fp, seq)
         elif kind == "layered":

@@ -79,6 +79,7 @@ def test_argument_validation_without_gpu():
     assert lib.kvs_set_budget(None, 1.0) == _lib.KVS_ERR_INVALID
     assert lib.kvs_set_budget_share(None, 1, 10.0) == _lib.KVS_ERR_INVALID
     assert lib.kvs_set_pace_burst(None, 1, 1 << 20) == _lib.KVS_ERR_INVALID
+    assert lib.kvs_set_staging(None, 64 << 20, 4) == _lib.KVS_ERR_INVALID
     assert lib.kvs_set_path(None, 0, 0, 0, 0) == _lib.KVS_ERR_INVALID
     s, r = (ctypes.c_uint64 * 2)(), ctypes.c_uint64()
     sms = (ctypes.c_int * 2)()

@@ -153,7 +153,7 @@ def main():
              ("in2x256", "in", (2, 256), 0.0, "kernel"),
              ("out8x512p52", "out", (8, 512), 52.0, "kernel"),
              ("out8x512p20", "out", (8, 512), 20.0, "kernel"),
-             ("ce_batch_in", "in", (8, 256), 0.0, "ce_batch")]
+             ("ce_staged_in", "in", (8, 256), 0.0, "ce_staged")]
     sel = os.environ.get("SWAPS")
     if sel:
         swaps = [s for s in swaps if s[0] in sel.split(",")]

@@ -76,7 +76,7 @@ def main():
             row["total_gbs"] = round(2 * args.reps * nbytes / max(t_out, t_in) / 1e9, 2)
             res.append(row)
             print(json.dumps(row), flush=True)
-    for mode, name in ((1, "ce_per_run"), (2, "ce_batch")):
+    for mode, name in ((1, "ce_per_run"), (2, "ce_staged")):
         t_out, t_in = run_pair(lambda: dp.baseline("out", mode, ops_out, stream=s_out),
                                lambda: dp.baseline("in", mode, ops_in, stream=s_in),
                                s_out, s_in, args.reps)

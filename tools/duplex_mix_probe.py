@@ -1,6 +1,6 @@
 """Full-duplex mixes: which engine per direction reaches the most combined
 host-link GB/s when a swap-out and a swap-in run at once (LSU kernel, TMA
-bulk kernel, copy-engine batch)."""
+bulk kernel, copy-engine staged path)."""
 
 import json
 import sys

@@ -22,22 +22,16 @@ from paper_2411_18424_b200.geometry import LLAMA3_8B  # noqa: E402
 from paper_2411_18424_b200.swap import DUPLEX_POLICIES  # noqa: E402
 
 EXTRA = {
-    "mix_lsu8_cebatch": {"out": (8, 512, 0.0), "in": (8, 512, 0.0), "budget": 0.0,
-                         "engine": {"in": "ce_batch"}, "signals": "plan"},
-    "mix_lsu32_cebatch": {"out": (32, 512, 0.0), "in": (8, 512, 0.0), "budget": 0.0,
-                          "engine": {"in": "ce_batch"}, "signals": "plan"},
-    "mix_lsu16_cerun": {"out": (16, 512, 0.0), "in": (8, 512, 0.0), "budget": 0.0,
-                        "engine": {"in": "ce_per_run"}, "signals": "plan"},
-    "mix_lsu32_cerun": {"out": (32, 512, 0.0), "in": (8, 512, 0.0), "budget": 0.0,
-                        "engine": {"in": "ce_per_run"}, "signals": "plan"},
-    "mix_bulk_cebatch": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0,
-                         "path": "bulk", "engine": {"in": "ce_batch"}, "signals": "plan"},
-    "mix_cerun_lsu": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0,
-                      "engine": {"out": "ce_per_run"}, "signals": "plan"},
+    "mix_lsu16_cestaged": {"out": (16, 512, 0.0), "in": (8, 512, 0.0), "budget": 0.0,
+                           "engine": {"in": "ce_staged"}, "signals": "plan"},
+    "mix_cestaged_bulk": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0,
+                          "path": "bulk", "engine": {"out": "ce_staged"}, "signals": "plan"},
+    "mix_cestaged_lsu": {"out": (8, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0,
+                         "engine": {"out": "ce_staged"}, "signals": "plan"},
+    "mix_bulk_cerun": {"out": (64, 0, 0.0), "in": (64, 0, 0.0), "budget": 0.0,
+                       "path": "bulk", "engine": {"in": "ce_per_run"}, "signals": "plan"},
     "ce_run_both": {"out": (8, 512, 0.0), "in": (8, 512, 0.0), "budget": 0.0,
                     "engine": {"out": "ce_per_run", "in": "ce_per_run"}, "signals": "plan"},
-    "lsu_both_32": {"out": (32, 512, 0.0), "in": (32, 512, 0.0), "budget": 0.0,
-                    "signals": "plan"},
 }
 
 
@@ -52,7 +46,8 @@ def main():
     dp = SwapDataPlane(cache, host)
     cache.planes.view(torch.int32).random_()
     out = {"group": args.group, "plan_blocks": args.plan_blocks, "runs": {}}
-    names = os.environ.get("POLICIES", ",".join(["throughput", "throughput_mix", *EXTRA]))
+    names = os.environ.get("POLICIES", ",".join(["throughput", "throughput_mix",
+                                                  "throughput_staged", *EXTRA]))
     for group in [int(g) for g in os.environ.get("GROUPS", "16").split(",")]:
         args.group = group
         for name in names.split(","):

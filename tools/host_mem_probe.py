@@ -76,7 +76,7 @@ def main():
         row["ce_per_run"] = {"out": round(nbytes / t_out / 1e9, 2), "in": round(nbytes / t_in / 1e9, 2)}
         t_o, t_i = timed([(s1, lambda: dp.baseline("out", 2, ops_a, stream=s1)),
                           (s2, lambda: dp.baseline("in", 2, ops_b, stream=s2))])
-        row["duplex_ce_batch"] = {"out": round(hb / t_o / 1e9, 2), "in": round(hb / t_i / 1e9, 2)}
+        row["duplex_ce_staged"] = {"out": round(hb / t_o / 1e9, 2), "in": round(hb / t_i / 1e9, 2)}
         # exact round trip through this pool (checked on the GPU: no CPU reads of WC memory)
         dp.set_launch("out", 0, 0)
         dp.set_launch("in", 0, 0)

@@ -78,7 +78,7 @@ def main():
     print(json.dumps(results), flush=True)
 
     # (label, path, {dir: (ctas, threads)}, {dir: pace GB/s}, impl, dirs)
-    # impl: kernel | ce_batch | ce_per_run
+    # impl: kernel | ce_staged | ce_per_run
     sweep = os.environ.get("SWEEP", "in")
     configs = []
     if sweep == "probe":
@@ -137,10 +137,10 @@ def main():
                         {"out": 30.0, "in": 0.0}, "kernel", ("out",)))
         configs.append(("bulk_in8", "bulk", {"out": (8, 32), "in": (8, 32)},
                         {"out": 0.0, "in": 0.0}, "kernel", ("in",)))
-        configs.append(("ce_batch_in", "lsu", {"out": (8, 512), "in": (8, 256)},
-                        {"out": 0.0, "in": 0.0}, "ce_batch", ("in",)))
-        configs.append(("ce_batch_out", "lsu", {"out": (8, 512), "in": (8, 256)},
-                        {"out": 0.0, "in": 0.0}, "ce_batch", ("out",)))
+        configs.append(("ce_staged_in", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 0.0, "in": 0.0}, "ce_staged", ("in",)))
+        configs.append(("ce_staged_out", "lsu", {"out": (8, 512), "in": (8, 256)},
+                        {"out": 0.0, "in": 0.0}, "ce_staged", ("out",)))
     elif sweep == "burst":
         # same mean swap-in rate, released steadily or in bursts (kvs_set_pace_burst)
         for pace in (10.0, 20.0, 40.0):
@@ -211,7 +211,7 @@ def main():
             if impl == "kernel":
                 dp.swap(d, ops, stream=st)
             else:
-                dp.baseline(d, 2 if impl == "ce_batch" else 1, ops, stream=st)
+                dp.baseline(d, 2 if impl == "ce_staged" else 1, ops, stream=st)
             e1.record(st)
             t[d] = (e0, e1)
         # decode steps while the swaps run (steps that start before the swaps end count)

@@ -1,6 +1,6 @@
 """Per-plan latency of the swap path: one plan of B blocks, end to end on its
 stream (launch + op-counter memset + kernel + flag publication), for the
-executor's kvs_swap_ops path, plain kvs_swap and the copy-engine batch call.
+executor's kvs_swap_ops path, plain kvs_swap and the staged copy-engine path.
 Small plans (TP8 shards, short contexts) are latency-, not bandwidth-bound.
 
 python tools/latency_probe.py --model llama3-70b --tp 8   -> one JSON line
@@ -44,7 +44,7 @@ def main():
             impls = {
                 "kernel_ops": lambda: dp.swap_ops(d, ops, flags.data_ptr(), 1, stream=s),
                 "kernel": lambda: dp.swap(d, ops, stream=s),
-                "ce_batch": lambda: dp.baseline(d, 2, ops, stream=s),
+                "ce_staged": lambda: dp.baseline(d, 2, ops, stream=s),
             }
             for name, fn in impls.items():
                 fn()

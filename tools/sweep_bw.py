@@ -80,7 +80,7 @@ def main():
                 if mode == 0 and g > 16:
                     continue
                 sec = timed(lambda: dp.baseline(d, mode, ops, stream=s), s, 1)
-                res.append(dict(group=g, dir=d, impl=["ce_per_block", "ce_per_run", "ce_batch"][mode],
+                res.append(dict(group=g, dir=d, impl=["ce_per_block", "ce_per_run", "ce_staged"][mode],
                                 gbs=nbytes / sec / 1e9))
                 print(json.dumps(res[-1]), flush=True)
     if args.no_duplex:
