@@ -98,8 +98,8 @@ def parse(argv=None):
     ap.add_argument("--serving-policy", default="serving",
                     help="StreamExecutor duplex policy of the live traces' FastSwitch arm")
     ap.add_argument("--control-plane", default="native", choices=["native", "python"],
-                    help="live traces: the C++ control plane (native_ctrl) or the Python "
-                         "one (same decisions)")
+                    help="e2e legs and live traces: the C++ control plane (native_ctrl) or "
+                         "the Python one (same decisions)")
     ap.add_argument("--stream-decode", action="store_true",
                     help="live traces / serving: launch decode kernels one by one instead "
                          "of as one CUDA graph per step")
@@ -689,6 +689,8 @@ def run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, policy):
                for d in ("out", "in")}
     mgr = SwapManager(TransferParams(), bytes_per_block=geo.block_bytes, executor=ex)
     gpu_pool, host_pool = pools(args.plan_blocks)
+    if args.control_plane == "native":  # the same API on the C++ control plane
+        from paper_2411_18424_b200.native_ctrl import NativeCpuStore as CpuStore  # noqa: F811
     store = CpuStore(host_pool, reuse_enabled=True)
     n_req = 64
     per = max(1, args.plan_blocks // n_req)
@@ -754,6 +756,7 @@ def run_e2e(args, geo, dp, dev, barrier, max_over_ranks, world, policy):
             "api": f"CpuStore.plan_swap_out/plan_swap_in -> SwapManager.dispatch -> "
                    f"StreamExecutor ({policy} policy) -> kvs_swap / kvs_memcpy_baseline "
                    f"(C ABI); wall clock incl. planning and sync",
+            "control_plane": args.control_plane,
             "requests_per_step": n_req, "gpu_launches": launches,
             "bytes_verified": verified}
 
