@@ -809,7 +809,11 @@ __global__ void __launch_bounds__(512) kvs_stage_kernel(const __grid_constant__ 
 }
 
 void stage_release(KvsHandle* h, int dir) {
+  // Slot users run on the aux stream and on callers' streams (the copies):
+  // the last record of every ring event marks a slot's last use.
   if (h->stage_aux[dir]) cudaStreamSynchronize(h->stage_aux[dir]);
+  for (cudaEvent_t e : h->stage_filled[dir]) cudaEventSynchronize(e);
+  for (cudaEvent_t e : h->stage_free[dir]) cudaEventSynchronize(e);
   if (h->d_stage[dir]) cudaFree(h->d_stage[dir]);
   for (cudaEvent_t e : h->stage_filled[dir]) cudaEventDestroy(e);
   for (cudaEvent_t e : h->stage_free[dir]) cudaEventDestroy(e);

@@ -1,7 +1,7 @@
 """Summarise an ncu --set full capture of the kvs_swap kernels into
 profiles/ncu_kernel_summary.json (+ a markdown table on stdout).
 
-python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--launch-csv gpurun_out/launches.csv]
+python tools/ncu_summary.py gpurun_out/prof.ncu-rep [output name under profiles/]
 """
 
 import csv
