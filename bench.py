@@ -835,6 +835,7 @@ def run_trace(args, geo, dev, name):
                             "swap_gib": {"out": round(st["bytes_out"] / 2**30, 2),
                                          "in": round(st["bytes_in"] / 2**30, 2)},
                             "swap_rates": rt.swap_rates(),
+                            "iteration_anatomy": eng.iteration_anatomy(),
                             "kernel_launches": st["kernel_launches"]}
         rt.close()
     del decode

@@ -769,6 +769,21 @@ class LiveEngine(Engine):
             "overall_mean_cpu_ms": sum(t[1] for t in self._trace) / len(self._trace) / 1e3,
         }
 
+    def iteration_anatomy(self) -> dict:
+        """Where a computing iteration's wall time goes, on average (ms): host
+        scheduling; the runtime's host-side launches (decode step capture +
+        graph update + KV append); on the device, the interval from the
+        iteration's first GPU-side wait to the decode step's start (host
+        launch latency or conflict / sync-swap-in waits, whichever is longer)
+        and the decode step itself.  TBT is one iteration per token."""
+        if not self._trace:
+            return {}
+        n = len(self._trace)
+        mean = lambda i, scale: round(sum(t[i] for t in self._trace) / n * scale, 4)  # noqa: E731
+        return {"iterations": n, "mean_ms": mean(0, 1e-3), "schedule_ms": mean(1, 1e-3),
+                "launch_ms": mean(9, 1e-3), "pre_decode_device_ms": mean(2, 1.0),
+                "decode_ms": mean(3, 1.0)}
+
     def latency_summary(self) -> dict:
         def pct(xs, q):
             return percentile(xs, q) / 1e3 if xs else None

@@ -63,6 +63,7 @@ def run_one(args, mode, impl, decode, geo):
         "control_plane": args.control_plane,
         "graph_stats": eng.graph.stats() if eng.graph is not None else None,
         "latency": lat,
+        "iteration_anatomy": eng.iteration_anatomy(),
         "swap_rates": rt.swap_rates(),
         "report": {k: v for k, v in rep.to_dict().items() if k != "granularity_histogram"},
         "swap": {d: {"bytes": nbytes[d], "gbs_while_busy": round(nbytes[d] / secs[d] / 1e9, 2)
