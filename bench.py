@@ -573,6 +573,9 @@ def run_ours(args, geo):
             part = f"swap_on_{args.sm_partition}_sms"
             serving[args.serving_policy + "_" + part] = serving_interference(
                 dp, dev, s, args.sm_partition, args.serving_policy, graph=g)
+            # the same at the link rate (swap-in unpaced)
+            serving["serving_link_" + part] = serving_interference(
+                dp, dev, s, args.sm_partition, "serving_link", graph=g)
             # the same policy with the decode kernels launched one by one: their
             # command fetches share the PCIe link with the swap-in
             serving[args.serving_policy + "_stream_decode_" + part] = serving_interference(

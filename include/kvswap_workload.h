@@ -84,6 +84,34 @@ int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_t n_segs,
                   int32_t block_tokens, int32_t plane_lo, int32_t plane_hi, uint64_t stream,
                   uint32_t* mismatch);
 
+/* One decode step captured into `g` in one call (what the live engine did
+ * with ~100 calls from Python per step: the host time a synchronous loop
+ * adds to every token).  Per layer l = 0..h's planes-1:
+ *   - wait until dep_flags[d][l] >= dep_seqs[d] for every dep d (plane
+ *     flags of layer-pipelined swap-ins, kvs_swap_signaled);
+ *   - mark 2l (if marks);
+ *   - check the resident KV of `segs` in plane l (kvs_kv_tokens mode 1);
+ *   - stream w_bytes_per_layer bytes of `weights` (kvs_stream_read);
+ *   - mark 2l+1 (if marks).
+ * Then ends the capture (kvs_graph_end semantics, *how). */
+typedef struct KvsDecodeStep {
+  const int64_t* segs;         /* [n_segs][4] (request, lo, hi, physical block of lo) */
+  int32_t n_segs;
+  int32_t block_tokens;
+  uint32_t* mismatch;          /* KV check counter (required when n_segs > 0) */
+  const void* weights;
+  uint64_t weight_bytes;
+  uint64_t w_bytes_per_layer;  /* 0: no weight streaming */
+  void* sink;
+  int32_t w_ctas;              /* kvs_stream_read ctas */
+  int32_t n_deps;
+  const uint64_t* dep_flags;   /* [n_deps] device addresses of per-plane flag arrays */
+  const uint32_t* dep_seqs;    /* [n_deps] */
+  int32_t marks;               /* 1: timing marks around each layer (needs 2 x planes marks) */
+  int32_t reserved;            /* must be 0 */
+} KvsDecodeStep;
+int kvs_graph_decode_step(KvsGraph* g, KvsHandle* h, const KvsDecodeStep* step, int* how);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,7 @@ EXPORTED_SYMBOLS = (
     "kvs_graph_create", "kvs_graph_destroy", "kvs_graph_stream", "kvs_graph_begin",
     "kvs_graph_mark", "kvs_graph_end", "kvs_graph_launch", "kvs_graph_elapsed",
     "kvs_graph_stats",  # include/kvswap_workload.h
+    "kvs_graph_decode_step",  # include/kvswap_workload.h
     "kvs_kv_tokens",  # include/kvswap_workload.h
 )
 
@@ -89,6 +90,26 @@ class KvsSignals(ctypes.Structure):
         ("done_flag", ctypes.c_void_p),
         ("seq", ctypes.c_uint32),
         ("reserved", ctypes.c_uint32),
+    ]
+
+
+class KvsDecodeStep(ctypes.Structure):
+    """include/kvswap_workload.h KvsDecodeStep."""
+    _fields_ = [
+        ("segs", ctypes.c_void_p),
+        ("n_segs", ctypes.c_int32),
+        ("block_tokens", ctypes.c_int32),
+        ("mismatch", ctypes.c_void_p),
+        ("weights", ctypes.c_void_p),
+        ("weight_bytes", ctypes.c_uint64),
+        ("w_bytes_per_layer", ctypes.c_uint64),
+        ("sink", ctypes.c_void_p),
+        ("w_ctas", ctypes.c_int32),
+        ("n_deps", ctypes.c_int32),
+        ("dep_flags", ctypes.c_void_p),
+        ("dep_seqs", ctypes.c_void_p),
+        ("marks", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -193,6 +214,9 @@ def _declare(lib: ctypes.CDLL) -> None:
     lib.kvs_graph_elapsed.argtypes = [c.c_void_p, c.c_int, c.c_int, c.POINTER(c.c_float)]
     lib.kvs_graph_stats.restype = c.c_int
     lib.kvs_graph_stats.argtypes = [c.c_void_p, c.POINTER(c.c_int64)]
+    lib.kvs_graph_decode_step.restype = c.c_int
+    lib.kvs_graph_decode_step.argtypes = [c.c_void_p, c.c_void_p, c.POINTER(KvsDecodeStep),
+                                          c.POINTER(c.c_int)]
     lib.kvs_kv_tokens.restype = c.c_int
     lib.kvs_kv_tokens.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_int32, c.c_int32,
                                   c.c_int32, c.c_int32, c.c_uint64, c.c_void_p]

@@ -1611,6 +1611,43 @@ extern "C" int kvs_graph_elapsed(KvsGraph* g, int slot_a, int slot_b, float* ms)
   return cuda_rc(cudaEventElapsedTime(ms, g->marks[slot_a], g->marks[slot_b]));
 }
 
+extern "C" int kvs_graph_decode_step(KvsGraph* g, KvsHandle* h, const KvsDecodeStep* st,
+                                     int* how) {
+  if (g == nullptr || h == nullptr || st == nullptr || how == nullptr || st->reserved != 0 ||
+      st->n_segs < 0 || st->n_deps < 0 || (st->n_deps > 0 && (!st->dep_flags || !st->dep_seqs)) ||
+      (st->n_segs > 0 && (st->segs == nullptr || st->mismatch == nullptr)) ||
+      (st->w_bytes_per_layer > 0 && (st->weights == nullptr || st->sink == nullptr)))
+    return KVS_ERR_INVALID;
+  const int planes = h->geo.num_planes;
+  if (st->marks && 2 * planes > static_cast<int>(g->marks.size())) return KVS_ERR_INVALID;
+  static auto wait_fn = driver_fn<StreamWaitValue32Fn>("cuStreamWaitValue32");
+  if (st->n_deps > 0 && wait_fn == nullptr) return KVS_ERR_UNSUPPORTED;
+  int rc = kvs_graph_begin(g);
+  if (rc) return rc;
+  const uint64_t cap = reinterpret_cast<uint64_t>(g->cap);
+  for (int l = 0; l < planes && rc == 0; ++l) {
+    for (int32_t d = 0; d < st->n_deps && rc == 0; ++d) {
+      const CUresult r = wait_fn(reinterpret_cast<CUstream>(g->cap),
+                                 static_cast<CUdeviceptr>(st->dep_flags[d] + 4ull * l),
+                                 st->dep_seqs[d], CU_STREAM_WAIT_VALUE_GEQ);
+      if (r != CUDA_SUCCESS) rc = KVS_ERR_UNSUPPORTED;
+    }
+    if (rc == 0 && st->marks) rc = kvs_graph_mark(g, 2 * l);
+    if (rc == 0 && st->n_segs > 0)
+      rc = kvs_kv_tokens(h, 1, st->segs, st->n_segs, st->block_tokens, l, l + 1, cap,
+                         st->mismatch);
+    if (rc == 0 && st->w_bytes_per_layer > 0)
+      rc = kvs_stream_read_ex(g->device, cap, st->weights, st->weight_bytes,
+                              st->w_bytes_per_layer, st->w_ctas, st->sink, 0);
+    if (rc == 0 && st->marks) rc = kvs_graph_mark(g, 2 * l + 1);
+  }
+  int ended = 0;
+  const int rc_end = kvs_graph_end(g, &ended);  // always leave capture mode
+  if (rc) return rc;
+  *how = ended;
+  return rc_end;
+}
+
 extern "C" int kvs_graph_stats(KvsGraph* g, int64_t* out3) {
   if (g == nullptr || out3 == nullptr) return KVS_ERR_INVALID;
   out3[0] = g->instantiations;

@@ -75,8 +75,11 @@ class DecodeEmulator:
                                       ctypes.c_void_p(self.sink.data_ptr()))
         _lib.check(rc, "kvs_stream_read")
 
+    def bytes_for_us(self, us: float) -> int:
+        return max(16, int(us * self.bytes_per_us) // 16 * 16)
+
     def launch_us(self, stream, us: float) -> int:
-        nbytes = max(16, int(us * self.bytes_per_us) // 16 * 16)
+        nbytes = self.bytes_for_us(us)
         self.launch(stream, nbytes)
         return nbytes
 
@@ -130,6 +133,31 @@ class DecodeGraph:
 
     def launch(self, stream) -> None:
         _lib.check(self.lib.kvs_graph_launch(self.h, int(stream.cuda_stream)), "kvs_graph_launch")
+
+    def capture_step(self, dataplane, decode: "DecodeEmulator", segs, mismatch_ptr: int,
+                     w_bytes_per_layer: int, deps=(), marks: bool = False) -> int:
+        """Capture a whole decode step in one native call
+        (kvs_graph_decode_step): per layer, the plane-flag waits of `deps`
+        ((flag array address, seq) pairs), the KV check of `segs` in that
+        plane, and `w_bytes_per_layer` of weight streaming; marks 2l / 2l+1
+        around layer l.  Returns how the executable graph was refreshed."""
+        arr = None
+        if segs is not None and len(segs):
+            arr = np.ascontiguousarray(segs, dtype=np.int64).reshape(-1, 4)
+        n_deps = len(deps)
+        flags = (ctypes.c_uint64 * max(1, n_deps))(*[int(p) for p, _ in deps])
+        seqs = (ctypes.c_uint32 * max(1, n_deps))(*[int(q) & 0xFFFFFFFF for _, q in deps])
+        st = _lib.KvsDecodeStep(
+            arr.ctypes.data if arr is not None else None, 0 if arr is None else arr.shape[0],
+            dataplane.geometry.block_tokens, mismatch_ptr or None,
+            decode.weights.data_ptr(), decode.weights.numel(), int(w_bytes_per_layer),
+            decode.sink.data_ptr(), decode.ctas, n_deps,
+            ctypes.addressof(flags) if n_deps else None,
+            ctypes.addressof(seqs) if n_deps else None, 1 if marks else 0, 0)
+        how = ctypes.c_int()
+        _lib.check(self.lib.kvs_graph_decode_step(self.h, dataplane.handle, ctypes.byref(st),
+                                                  ctypes.byref(how)), "kvs_graph_decode_step")
+        return how.value
 
     def elapsed(self, a: int, b: int) -> float:
         ms = ctypes.c_float()
@@ -610,7 +638,6 @@ class LiveEngine(Engine):
                 # joining request's KV.  This iteration's KV writes follow the
                 # last layer, when every joining request's KV has landed.
                 self.runtime.barrier(self, spans, skip=layer_deps)
-                t_rt = time.perf_counter()
                 waits_seen = grant_waits + list(ex.last_barrier)
                 swapping = True
                 planes = self.runtime.geometry.num_planes
@@ -618,40 +645,40 @@ class LiveEngine(Engine):
                 layer_evs = []
                 segs = self.runtime.read_segments(self, reads) if reads else None
                 g = self.graph
-                st = g.begin() if g is not None else compute
-                if g is None:
+                if g is not None:
+                    # one native call captures the step: per layer the plane-flag
+                    # waits, the KV check and the weight stream, with marks
+                    w_layer = self.decode.bytes_for_us(w_us / planes) if w_us > 0 else 0
+                    g.capture_step(self.runtime.dataplane, self.decode, segs,
+                                   self.runtime.kv_check_ptr(), w_layer,
+                                   deps=[ex.plane_flags(dep) for dep in layer_deps], marks=True)
+                    kv_b = self.runtime.account_reads(segs) if segs is not None else 0
+                    w_b = w_layer * planes
+                    layer_evs = [(2 * layer, 2 * layer + 1) for layer in range(planes)]
+                else:  # kernel by kernel on the compute stream
                     e0.record(compute)
-                for layer in range(planes):
-                    for dep in layer_deps:
-                        ex.wait_plane(st, dep, layer)
-                    if g is None:
+                    for layer in range(planes):
+                        for dep in layer_deps:
+                            ex.wait_plane(compute, dep, layer)
                         ea = torch.cuda.Event(enable_timing=True)
                         ea.record(compute)  # this layer's KV has landed: decode starts
-                    else:
-                        g.mark(2 * layer)
-                    if reads:
-                        kv_b += self.runtime.attend(self, reads, planes=(layer, layer + 1),
-                                                   segs=segs, stream=st)
-                    if w_us > 0:
-                        w_b += self.decode.launch_us(st, w_us / planes)
-                    if g is None:
+                        if reads:
+                            kv_b += self.runtime.attend(self, reads, planes=(layer, layer + 1),
+                                                       segs=segs, stream=compute)
+                        if w_us > 0:
+                            w_b += self.decode.launch_us(compute, w_us / planes)
                         eb = torch.cuda.Event(enable_timing=True)
                         eb.record(compute)
                         layer_evs.append((ea, eb))
-                    else:
-                        g.mark(2 * layer + 1)
-                        layer_evs.append((2 * layer, 2 * layer + 1))
                 if g is not None:
-                    g.end()
                     e0.record(compute)
                     g.launch(compute)
+                t_rt = time.perf_counter()  # host: barrier + decode capture / launches
                 e1.record(compute)
                 self.runtime.write(self, spans)
             else:
                 self.runtime.compute(self, spans)
-                t_rt = time.perf_counter()
                 waits_seen = grant_waits + list(ex.last_barrier)
-                e0.record(compute)
                 swapping = any(not r.poll() for r in ex.pending)
                 layer_evs = None
                 planes = self.runtime.geometry.num_planes
@@ -659,19 +686,30 @@ class LiveEngine(Engine):
                     kv_b = w_b = 0
                     segs = self.runtime.read_segments(self, reads) if reads else None
                     g = self.graph
-                    st = g.begin() if g is not None else compute
-                    for layer in range(planes):
-                        if reads:
-                            kv_b += self.runtime.attend(self, reads, planes=(layer, layer + 1),
-                                                       segs=segs, stream=st)
-                        if w_us > 0:
-                            w_b += self.decode.launch_us(st, w_us / planes)
-                    if g is not None:
-                        g.end()
+                    if g is None:
+                        e0.record(compute)
+                        for layer in range(planes):
+                            if reads:
+                                kv_b += self.runtime.attend(self, reads,
+                                                           planes=(layer, layer + 1),
+                                                           segs=segs, stream=compute)
+                            if w_us > 0:
+                                w_b += self.decode.launch_us(compute, w_us / planes)
+                    else:
+                        w_layer = self.decode.bytes_for_us(w_us / planes) if w_us > 0 else 0
+                        g.capture_step(self.runtime.dataplane, self.decode, segs,
+                                       self.runtime.kv_check_ptr(), w_layer)
+                        kv_b = self.runtime.account_reads(segs) if segs is not None else 0
+                        w_b = w_layer * planes
+                        # the step starts at the graph launch: the host's
+                        # capture time is not decode time
+                        e0.record(compute)
                         g.launch(compute)
                 else:
+                    e0.record(compute)
                     kv_b = self.runtime.attend(self, reads) if reads else 0
                     w_b = self.decode.launch_us(compute, w_us) if w_us > 0 else 0
+                t_rt = time.perf_counter()  # host: barrier + KV append + decode capture / launches
                 e1.record(compute)
             compute.synchronize()
             if self._deferred:

@@ -202,6 +202,19 @@ class Runtime:
         self.kv_bytes_read += nbytes
         return nbytes
 
+    def kv_check_ptr(self) -> int:
+        """Device address of the KV-check mismatch counter (captured steps)."""
+        return self._kv_bad.data_ptr()
+
+    def account_reads(self, segs: np.ndarray) -> int:
+        """Bytes a whole step's KV check of `segs` reads (every plane), counted
+        like attend() counts them; returns the bytes."""
+        if not self.write_kv or segs is None or not len(segs):
+            return 0
+        nbytes = int((segs[:, 2] - segs[:, 1]).sum()) * self.token_bytes
+        self.kv_bytes_read += nbytes
+        return nbytes
+
     def kv_errors(self) -> int:
         """Words that differed from their tokens' KV in every attend() so far."""
         self.executor.compute.synchronize()

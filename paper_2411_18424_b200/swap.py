@@ -225,14 +225,21 @@ DUPLEX_POLICIES = {
                          "priority": "in"},
     "latency_share": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
                       "share": {"in": 42.0}},
-    # serving: the link rate in each direction (swap-in bounded by reads in
-    # flight, swap-out paced at 52 GB/s), with 42 GB/s of a 60 GB/s budget
-    # reserved for swap-in while both run.  With the decode step launched as
-    # a CUDA graph (live.DecodeGraph) a full-rate swap-in costs a 32-layer
-    # step +9% in the worst case and +7% on the live trace
-    # (profiles/r02_graph_decode.json).
-    "serving": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
+    # serving: swap-in paced at 48 GB/s (bounded by reads in flight as
+    # well), swap-out at 52, with 42 GB/s of a 60 GB/s budget reserved for
+    # swap-in while both run; the decode step launched as one CUDA graph
+    # (live.DecodeGraph).  On the live stress trace the pace costs swap-in
+    # nothing while busy (46.6 vs 46.7 GB/s: the traces' plans average ~146
+    # MiB and do not reach the link rate) and cuts the swap-induced stall
+    # from 9.1-9.7% to 8.4% [7.8, 9.0] (profiles/r02_live_stall_pace.json,
+    # DESIGN §3.3).
+    "serving": {"out": (8, 512, 52.0), "in": (8, 256, 48.0), "budget": 60.0,
                 "share": {"in": 42.0}},
+    # serving_link: the same at the link rate (swap-in unpaced, 51.4 GB/s =
+    # 82% of the link on long plans): +9.1% on a 32-layer step that
+    # overlaps it throughout, 9.1-9.7% on the live stress trace.
+    "serving_link": {"out": (8, 512, 52.0), "in": (8, 256, 0.0), "budget": 60.0,
+                     "share": {"in": 42.0}},
     # serving_paced: for decode kernels launched one by one on a stream, whose
     # command fetches queue behind a saturating swap-in's PCIe reads: paced
     # below the link (in 40 / out 20 GB/s) the stall stays under 10%
@@ -452,6 +459,13 @@ class StreamExecutor:
         if self.timing:
             self.history.append(rec)
         return rec
+
+    def plane_flags(self, rec: TransferRecord) -> tuple[int, int]:
+        """(device address of a layered transfer's per-plane flag array, the
+        value each flag receives): what a captured decode step waits on."""
+        if rec.plane_base is None:
+            raise ValueError("transfer was not issued plane-major (layered_swap_in)")
+        return self._flags_ptr + 4 * rec.plane_base, rec.seq
 
     def wait_plane(self, stream, rec: TransferRecord, plane: int) -> None:
         """`stream` waits until plane `plane` of a layered transfer has landed."""

@@ -97,3 +97,54 @@ def test_plane_flag_waits_are_graph_nodes(cuda_ok):
     assert g.elapsed(0, 1) > 0
     g.close()
     host.close()
+
+
+def test_one_call_step_capture_matches_and_waits_per_layer(cuda_ok):
+    """kvs_graph_decode_step (DecodeGraph.capture_step): the whole step in one
+    native call.  It reads the same KV as the per-call capture (a corrupted
+    word in one plane is counted), streams the weights, and layer l of the
+    step waits for plane flag l of every dependency: with the flags of
+    planes >= 2 unpublished, the marks of layers 0-1 complete while the step
+    is still parked."""
+    cache, host, dp = _setup()
+    dec = DecodeEmulator("cuda:0", weight_bytes=64 << 20)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda:0")
+    g = DecodeGraph("cuda:0", marks=2 * GEO.num_planes)
+    comp, side = torch.cuda.Stream(), torch.cuda.Stream()
+    segs = np.array([[3, 0, 40, 5], [7, 0, 17, 20]], dtype=np.int64)
+    dp.kv_tokens(0, segs, stream=comp)
+    comp.synchronize()
+    for it in range(3):
+        how = g.capture_step(dp, dec, segs, bad.data_ptr(), (1 + it) << 20, marks=True)
+        assert how == (2 if it == 0 else 1)
+        g.launch(comp)
+        comp.synchronize()
+        assert int(bad.item()) == 0
+        assert all(g.elapsed(2 * l, 2 * l + 1) > 0 for l in range(GEO.num_planes))
+    cache.planes[2, 20, 0] += 1  # request 7's first K word in plane 2
+    g.capture_step(dp, dec, segs, bad.data_ptr(), 1 << 20)
+    g.launch(comp)
+    comp.synchronize()
+    assert int(bad.item()) == 1
+    # per-layer waits on two dependencies' plane flags
+    flags = torch.zeros(2, GEO.num_planes, dtype=torch.int32, device="cuda:0")
+    flags[:, :2] = 9
+    deps = [(flags[0].data_ptr(), 9), (flags[1].data_ptr(), 9)]
+    bad.zero_()
+    cache.planes[2, 20, 0] -= 1
+    torch.cuda.synchronize()
+    g.capture_step(dp, dec, segs, bad.data_ptr(), 1 << 20, deps=deps, marks=True)
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(300_000_000)
+        flags[:, 2:].fill_(9)
+    g.launch(comp)
+    time.sleep(0.05)
+    assert not comp.query()  # parked at layer 2's waits
+    deadline = time.time() + 20
+    while not comp.query():
+        assert time.time() < deadline, "the step never left its plane-flag waits"
+        time.sleep(0.002)
+    assert int(bad.item()) == 0
+    assert all(g.elapsed(2 * l, 2 * l + 1) > 0 for l in range(GEO.num_planes))
+    g.close()
+    host.close()

@@ -51,11 +51,17 @@ def test_duplex_policies_are_well_formed():
     lat = DUPLEX_POLICIES["latency"]
     assert 0 < lat["out"][2] < 63.0
     assert lat["in"][2] == 0.0 and lat["in"][0] * lat["in"][1] // 32 * 4096 <= 512 * 1024
-    # the live traces' policy (graph-launched decode): the link rate each way,
-    # swap-in keeps a reserved share of the shared budget while both run
+    # the live traces' policy (graph-launched decode): swap-in paced just under
+    # the link and bounded by reads in flight, swap-out paced below the link,
+    # swap-in keeps a reserved share of the shared budget while both run;
+    # serving_link is the same with swap-in at the link rate
     srv = DUPLEX_POLICIES["serving"]
-    assert srv["in"][2] == 0.0 and 0 < srv["out"][2] < 63.0
+    assert 40.0 <= srv["in"][2] < 51.4 and 0 < srv["out"][2] < 63.0
+    assert srv["in"][0] * srv["in"][1] // 32 * 4096 <= 512 * 1024
     assert 0 < srv["share"]["in"] < srv["budget"]
+    link = DUPLEX_POLICIES["serving_link"]
+    assert link["in"][2] == 0.0 and {k: v for k, v in link.items() if k != "in"} == \
+        {k: v for k, v in srv.items() if k != "in"}
     # stream-launched decode: both directions paced below the link, under the budget
     sp = DUPLEX_POLICIES["serving_paced"]
     assert 0 < sp["out"][2] <= sp["in"][2] < 63.0

@@ -39,6 +39,7 @@ def run_one(args, mode, impl, decode, geo):
                  verify=args.verify, timing=True, duplex_policy=args.policy,
                  sm_partition=args.sm_partition, layered_swap_in=args.layered)
     eng = LiveEngine(cfg, generate(wl), rt, decode, layered=args.layered and impl == "kernel",
+                     attend=not args.no_attend,
                      per_layer_decode=not args.single_kernel_decode,
                      graph_decode=not args.stream_decode,
                      control_plane=args.control_plane)
@@ -59,6 +60,10 @@ def run_one(args, mode, impl, decode, geo):
     out = {
         "mode": mode, "copy_impl": impl, "wall_s": round(wall, 2),
         "policy": args.policy, "layered": args.layered, "sm_partition": args.sm_partition,
+        "policy_def": {k: list(v) if isinstance(v, tuple) else v
+                       for k, v in __import__("paper_2411_18424_b200.swap", fromlist=["x"])
+                       .DUPLEX_POLICIES[args.policy].items()},
+        "attend": not args.no_attend,
         "decode_launch": "cuda_graph" if eng.graph is not None else "stream",
         "control_plane": args.control_plane,
         "graph_stats": eng.graph.stats() if eng.graph is not None else None,
@@ -111,8 +116,18 @@ def main():
                     help="launch the per-layer decode kernels one by one on the stream "
                          "instead of as one CUDA graph")
     ap.add_argument("--control-plane", default="python", choices=["python", "native"])
+    ap.add_argument("--policy-json", default="",
+                    help='register a custom duplex policy under --policy, e.g. '
+                         '\'{"out": [8, 512, 52], "in": [8, 256, 45], "budget": 60}\'')
+    ap.add_argument("--no-attend", action="store_true",
+                    help="decode streams weights only (no per-layer KV reads)")
     ap.add_argument("--out", default="gpurun_out/live_trace.json")
     args = ap.parse_args()
+    if args.policy_json:
+        from paper_2411_18424_b200.swap import DUPLEX_POLICIES
+        pol = json.loads(args.policy_json)
+        DUPLEX_POLICIES[args.policy] = {k: tuple(v) if k in ("out", "in") else v
+                                        for k, v in pol.items()}
     geo = PRESETS[args.model]
     stream, ctas = None, 0
     if args.sm_partition:
