@@ -1665,8 +1665,10 @@ extern "C" int kvs_graph_stats(KvsGraph* g, int64_t* out3) {
 namespace {
 
 constexpr int kTokSegsMax = 256;
+constexpr int kTokSegsSmall = 32;  // size class for typical batches: 8x smaller params
 
-struct TokSegs {
+template <int CAP>
+struct TokSegsT {
   const uint64_t* planes;
   int64_t stride;          // plane_block_stride
   uint32_t plane_lo;       // planes [plane_lo, plane_lo + n_planes)
@@ -1676,11 +1678,35 @@ struct TokSegs {
   uint32_t n_segs;
   uint32_t* mismatch;      // mode 1: count of mismatching words
   int32_t mode;            // 0 write, 1 check
-  uint32_t seg_req[kTokSegsMax];
-  int32_t seg_lo[kTokSegsMax];       // first token
-  int32_t seg_tok_end[kTokSegsMax];  // inclusive prefix sum of tokens
-  int32_t seg_phys[kTokSegsMax];     // physical block of token seg_lo
+  uint32_t seg_req[CAP];
+  int32_t seg_lo[CAP];       // first token
+  int32_t seg_tok_end[CAP];  // inclusive prefix sum of tokens
+  int32_t seg_phys[CAP];     // physical block of token seg_lo
 };
+using TokSegs = TokSegsT<kTokSegsMax>;
+
+// The first n segments of `big` in a smaller parameter block (a captured
+// graph node's parameters are copied at every update and uploaded at launch).
+template <int CAP>
+TokSegsT<CAP> shrink(const TokSegs& big, uint32_t n) {
+  TokSegsT<CAP> t;
+  t.planes = big.planes;
+  t.stride = big.stride;
+  t.plane_lo = big.plane_lo;
+  t.n_planes = big.n_planes;
+  t.block_tokens = big.block_tokens;
+  t.words = big.words;
+  t.n_segs = big.n_segs;
+  t.mismatch = big.mismatch;
+  t.mode = big.mode;
+  for (uint32_t i = 0; i < n; ++i) {
+    t.seg_req[i] = big.seg_req[i];
+    t.seg_lo[i] = big.seg_lo[i];
+    t.seg_tok_end[i] = big.seg_tok_end[i];
+    t.seg_phys[i] = big.seg_phys[i];
+  }
+  return t;
+}
 
 // Runtime._pattern restated in uint32 (identical mod 2^32).
 __device__ __forceinline__ uint32_t kv_word(uint32_t req, uint32_t tok, uint32_t plane,
@@ -1692,7 +1718,8 @@ __device__ __forceinline__ uint32_t kv_word(uint32_t req, uint32_t tok, uint32_t
 // allows (word counts % 4 == 0), else single words.  Mode 1 is the live
 // engine's attention stand-in: it reads every KV byte of the batch and counts
 // words that differ from what the tokens wrote.
-__global__ void __launch_bounds__(256) kvs_kv_tokens_kernel(const __grid_constant__ TokSegs s) {
+template <int CAP>
+__global__ void __launch_bounds__(256) kvs_kv_tokens_kernel(const __grid_constant__ TokSegsT<CAP> s) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
   const uint64_t nwarps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -1799,7 +1826,10 @@ extern "C" int kvs_kv_tokens(KvsHandle* h, int mode, const int64_t* segs, int32_
     const uint64_t rows_per_cta = 8ull * (upr >= 32 ? 1u : 32u / upr);  // 8 warps per CTA
     const uint64_t want = (rows + rows_per_cta - 1) / rows_per_cta;
     const int ctas = static_cast<int>(want < 1184 ? want : 1184);
-    kvs_kv_tokens_kernel<<<ctas, 256, 0, st>>>(s);
+    if (n <= static_cast<uint32_t>(kTokSegsSmall))
+      kvs_kv_tokens_kernel<kTokSegsSmall><<<ctas, 256, 0, st>>>(shrink<kTokSegsSmall>(s, n));
+    else
+      kvs_kv_tokens_kernel<kTokSegsMax><<<ctas, 256, 0, st>>>(s);
     rc = cuda_rc(cudaGetLastError());
     if (rc) return rc;
   }

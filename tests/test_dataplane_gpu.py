@@ -238,7 +238,15 @@ def test_done_flag_orders_streams(cuda_ok, path):
     host.close()
 
 
-@pytest.mark.parametrize("path", ["lsu", "bulk"])
+def _swap_path(dp, path, direction, ops, stream):
+    """One plan through the kernel (LSU / TMA bulk) or the staged copy-engine path."""
+    if path == "staged":
+        dp.baseline(direction, 2, ops, stream=stream)
+    else:
+        dp.swap(direction, ops, stream=stream)
+
+
+@pytest.mark.parametrize("path", ["lsu", "bulk", "staged"])
 def test_config1_round_trip_llama3_8b(cuda_ok, path):
     """BASELINE config 1 at full size: 64 requests, LLaMA-3-8B KV shape
     (2 MiB blocks), footprints U{1..128}, fragmented random block tables,
@@ -247,7 +255,7 @@ def test_config1_round_trip_llama3_8b(cuda_ok, path):
     from paper_2411_18424_b200.geometry import LLAMA3_8B
 
     G = C = 8192
-    cache, host, dp = _mk(torch, LLAMA3_8B, G, C, path=path)
+    cache, host, dp = _mk(torch, LLAMA3_8B, G, C, path="lsu" if path == "staged" else path)
     gen = torch.Generator(device="cuda:0").manual_seed(0)
     cache.planes.view(torch.int32).random_(generator=gen)
     rng = np.random.default_rng(0)
@@ -264,7 +272,7 @@ def test_config1_round_trip_llama3_8b(cuda_ok, path):
     for r in range(64):
         lo, hi = bounds[r], bounds[r + 1]
         out_plans.append(orc.table_to_ops(gpu_tab[lo:hi], cpu_tab[lo:hi]))
-        dp.swap("out", out_plans[-1], stream=s_out)
+        _swap_path(dp, path, "out", out_plans[-1], s_out)
     torch.cuda.synchronize()
     # The whole host image against the oracle (TransferOp semantics,
     # bytes_oracle.apply_plan): the block the oracle's bijection maps each GPU
@@ -285,7 +293,7 @@ def test_config1_round_trip_llama3_8b(cuda_ok, path):
     new_tab = orc.random_block_table(rng, total, G)
     for r in range(64):
         lo, hi = bounds[r], bounds[r + 1]
-        dp.swap("in", orc.table_to_ops(new_tab[lo:hi], cpu_tab[lo:hi]), stream=s_in)
+        _swap_path(dp, path, "in", orc.table_to_ops(new_tab[lo:hi], cpu_tab[lo:hi]), s_in)
     torch.cuda.synchronize()
     back = cache.planes[:, torch.from_numpy(new_tab).cuda()]
     assert torch.equal(back, original)
@@ -486,10 +494,12 @@ def test_pacing_and_shared_budget(cuda_ok, path):
 
 @pytest.mark.parametrize("model,tp", [("qwen2.5-32b", 2), ("qwen2.5-32b", 4),
                                       ("qwen2.5-32b", 8), ("llama3-70b", 8)])
-def test_tp_shard_shapes_vs_oracle(cuda_ok, model, tp):
+@pytest.mark.parametrize("path", ["lsu", "staged"])
+def test_tp_shard_shapes_vs_oracle(cuda_ok, model, tp, path):
     """BASELINE configs 4-5: per-rank KV shards (32 / 16 / 8 KiB chunks, 64-80
     planes), C5-like long runs; swap-out byte-exact vs the oracle, then
-    swap-in to a new table == the oracle's restatement of the same ops."""
+    swap-in to a new table == the oracle's restatement of the same ops, on
+    the kernel and on the staged copy-engine path."""
     torch = cuda_ok
     from paper_2411_18424_b200.geometry import PRESETS
 
@@ -501,7 +511,7 @@ def test_tp_shard_shapes_vs_oracle(cuda_ok, model, tp):
     cache.planes.copy_(torch.from_numpy(pattern))
     ops = orc.random_runs(rng, 600, 145, G, C)  # C5: mean 145 blocks per op
     host.array[:] = 0
-    dp.swap("out", ops)
+    _swap_path(dp, path, "out", ops, None)
     torch.cuda.synchronize()
     want = np.zeros((C, geo.block_bytes), dtype=np.uint8)
     orc.apply_plan("out", pattern, want, ops)
@@ -509,7 +519,7 @@ def test_tp_shard_shapes_vs_oracle(cuda_ok, model, tp):
     cache.planes.fill_(0xA5)
     torch.cuda.synchronize()
     in_ops = orc.random_runs(rng, 600, 37, G, C)
-    dp.swap("in", in_ops)
+    _swap_path(dp, path, "in", in_ops, None)
     torch.cuda.synchronize()
     want_planes = np.full_like(pattern, 0xA5)
     orc.apply_plan("in", want_planes, want, in_ops)
