@@ -1641,11 +1641,19 @@ extern "C" int kvs_graph_decode_step(KvsGraph* g, KvsHandle* h, const KvsDecodeS
                               st->w_bytes_per_layer, st->w_ctas, st->sink, 0);
     if (rc == 0 && st->marks) rc = kvs_graph_mark(g, 2 * l + 1);
   }
-  int ended = 0;
-  const int rc_end = kvs_graph_end(g, &ended);  // always leave capture mode
-  if (rc) return rc;
-  *how = ended;
-  return rc_end;
+  if (rc) {
+    // Leave capture mode and drop the partial step; the executable graph is
+    // dropped too, so a launch without a successful recapture fails loudly.
+    cudaGraph_t dead = nullptr;
+    g->capturing = false;
+    cudaStreamEndCapture(g->cap, &dead);
+    if (dead) cudaGraphDestroy(dead);
+    cudaGetLastError();
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    g->exec = nullptr;
+    return rc;
+  }
+  return kvs_graph_end(g, how);
 }
 
 extern "C" int kvs_graph_stats(KvsGraph* g, int64_t* out3) {

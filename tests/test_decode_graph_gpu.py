@@ -148,3 +148,31 @@ def test_one_call_step_capture_matches_and_waits_per_layer(cuda_ok):
     assert all(g.elapsed(2 * l, 2 * l + 1) > 0 for l in range(GEO.num_planes))
     g.close()
     host.close()
+
+
+def test_failed_step_capture_leaves_no_runnable_graph(cuda_ok):
+    """A capture that fails midway (a KV segment past the pool) raises, drops
+    the partial step and the executable graph (a launch then fails loudly),
+    and the next good capture instantiates afresh."""
+    cache, host, dp = _setup()
+    dec = DecodeEmulator("cuda:0", weight_bytes=64 << 20)
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda:0")
+    g = DecodeGraph("cuda:0", marks=2 * GEO.num_planes)
+    comp = torch.cuda.Stream()
+    good = np.array([[3, 0, 40, 5]], dtype=np.int64)
+    dp.kv_tokens(0, good, stream=comp)
+    comp.synchronize()
+    assert g.capture_step(dp, dec, good, bad.data_ptr(), 1 << 20) == 2
+    g.launch(comp)
+    comp.synchronize()
+    with pytest.raises(IndexError):
+        g.capture_step(dp, dec, np.array([[3, 0, 40, 63]], dtype=np.int64), bad.data_ptr(),
+                       1 << 20)
+    with pytest.raises(ValueError):
+        g.launch(comp)
+    assert g.capture_step(dp, dec, good, bad.data_ptr(), 1 << 20) == 2
+    g.launch(comp)
+    comp.synchronize()
+    assert int(bad.item()) == 0
+    g.close()
+    host.close()

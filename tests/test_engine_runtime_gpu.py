@@ -261,3 +261,37 @@ def test_native_control_plane_drives_real_bytes(cuda_ok):
         assert rt.verified > 0
         rt.close()
     assert reports["native"] == reports["python"]
+
+
+@pytest.mark.parametrize("n_segs", [31, 32, 33, 256, 257, 600])
+def test_kv_token_kernel_size_classes(cuda_ok, n_segs):
+    """kvs_kv_tokens across its parameter size classes (32 and 256 segments
+    per launch, more in several launches): n one-token segments on distinct
+    blocks written, checked exact, then one flipped word counted once."""
+    import numpy as np
+    import torch
+
+    from paper_2411_18424_b200.runtime import Runtime
+
+    G = 640
+    rt = Runtime(TINY, G, 8, verify=True)
+    rt.cache.planes.fill_(0)
+    segs = np.array([[7 + i, i % TINY.block_tokens, i % TINY.block_tokens + 1, i]
+                     for i in range(n_segs)], dtype=np.int64)
+    s = rt.executor.compute
+    rt.dataplane.kv_tokens(0, segs, stream=s)
+    rt._mismatch.zero_()
+    rt.dataplane.kv_tokens(1, segs, stream=s, mismatch_ptr=rt._mismatch.data_ptr())
+    s.synchronize()
+    assert int(rt._mismatch.item()) == 0
+    # every segment's row landed: block i holds request 7+i's token
+    assert int((rt.cache.planes[:, :n_segs] != 0).any(dim=-1).sum().item()) == \
+        TINY.num_planes * n_segs
+    last = n_segs - 1
+    rt._slots[0, last, 0, last % TINY.block_tokens, 0] ^= 1
+    torch.cuda.synchronize()
+    rt._mismatch.zero_()
+    rt.dataplane.kv_tokens(1, segs, stream=s, mismatch_ptr=rt._mismatch.data_ptr())
+    s.synchronize()
+    assert int(rt._mismatch.item()) == 1
+    rt.close()
