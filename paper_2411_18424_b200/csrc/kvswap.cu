@@ -1618,6 +1618,7 @@ extern "C" int kvs_graph_decode_step(KvsGraph* g, KvsHandle* h, const KvsDecodeS
       (st->n_segs > 0 && (st->segs == nullptr || st->mismatch == nullptr)) ||
       (st->w_bytes_per_layer > 0 && (st->weights == nullptr || st->sink == nullptr)))
     return KVS_ERR_INVALID;
+  if (g->device != h->device) return KVS_ERR_INVALID;
   const int planes = h->geo.num_planes;
   if (st->marks && 2 * planes > static_cast<int>(g->marks.size())) return KVS_ERR_INVALID;
   static auto wait_fn = driver_fn<StreamWaitValue32Fn>("cuStreamWaitValue32");

@@ -86,6 +86,10 @@ def test_argument_validation_without_gpu():
     assert lib.kvs_sm_partition(-1, 8, 2, 0, 0, s, ctypes.byref(r), sms) == _lib.KVS_ERR_INVALID
     assert lib.kvs_sm_partition(0, 8, 0, 0, 0, s, ctypes.byref(r), sms) == _lib.KVS_ERR_INVALID
     assert lib.kvs_kv_tokens(None, 0, None, 0, 16, 0, -1, 0, None) == _lib.KVS_ERR_INVALID
+    step = _lib.KvsDecodeStep()
+    how = ctypes.c_int()
+    assert lib.kvs_graph_decode_step(None, None, ctypes.byref(step), ctypes.byref(how)) == \
+        _lib.KVS_ERR_INVALID
 
 
 def test_check_maps_codes_to_reference_exceptions():
