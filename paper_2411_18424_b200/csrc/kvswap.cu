@@ -1500,6 +1500,7 @@ struct KvsGraph {
   cudaGraphExec_t exec = nullptr;
   std::vector<cudaEvent_t> marks;
   bool capturing = false;
+  size_t exec_nodes = 0, exec_edges = 0;  // shape of the graph `exec` came from
   int64_t instantiations = 0, updates = 0, launches = 0;
 };
 
@@ -1571,6 +1572,15 @@ extern "C" int kvs_graph_end(KvsGraph* g, int* how) {
     return rc;
   }
   *how = 0;
+  // A graph with another node / edge count cannot update in place: go
+  // straight to re-instantiation instead of provoking a failed update.
+  size_t nodes = 0, edges = 0;
+  cudaGraphGetNodes(graph, nullptr, &nodes);
+  cudaGraphGetEdges(graph, nullptr, nullptr, &edges);
+  if (g->exec != nullptr && (nodes != g->exec_nodes || edges != g->exec_edges)) {
+    cudaGraphExecDestroy(g->exec);
+    g->exec = nullptr;
+  }
   if (g->exec != nullptr) {
     cudaGraphExecUpdateResultInfo info{};
     if (cudaGraphExecUpdate(g->exec, graph, &info) == cudaSuccess) {
@@ -1587,6 +1597,8 @@ extern "C" int kvs_graph_end(KvsGraph* g, int* how) {
     if (rc == 0) {
       *how = 2;
       ++g->instantiations;
+      g->exec_nodes = nodes;
+      g->exec_edges = edges;
     } else {
       g->exec = nullptr;
     }

@@ -16,6 +16,13 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "reference: needs the kvswitch reference importable")
 
 
+def under_sanitizer() -> bool:
+    """True inside compute-sanitizer (timings and rates mean nothing there)."""
+    return ("CUDA_INJECTION64_PATH" in os.environ
+            or "NV_SANITIZER_INJECTION_PORT_BASE" in os.environ
+            or "sanitizer" in os.environ.get("NVTX_INJECTION64_PATH", ""))
+
+
 def reference_available() -> bool:
     return (REFERENCE_SRC / "kvswitch").is_dir()
 

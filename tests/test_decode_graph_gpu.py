@@ -13,6 +13,8 @@ from paper_2411_18424_b200.dataplane import HostKVPool, PagedKVCache, SwapDataPl
 from paper_2411_18424_b200.geometry import KVGeometry
 from paper_2411_18424_b200.live import DecodeEmulator, DecodeGraph
 
+from conftest import under_sanitizer  # noqa: E402
+
 pytestmark = pytest.mark.gpu
 
 GEO = KVGeometry("tiny-kv", num_layers=4, num_kv_heads=2, head_dim=8)  # 1 KiB chunks
@@ -91,7 +93,8 @@ def test_plane_flag_waits_are_graph_nodes(cuda_ok):
     while not comp.query():
         assert time.time() < deadline, "the graph never left its flag wait"
         time.sleep(0.002)
-    assert not early  # it was parked on the flag
+    if not under_sanitizer():  # compute-sanitizer skews the timing
+        assert not early  # it was parked on the flag
     torch.cuda.synchronize()
     assert int(cache.planes.view(torch.int32).abs().sum().item()) > 0
     assert g.elapsed(0, 1) > 0
@@ -139,7 +142,8 @@ def test_one_call_step_capture_matches_and_waits_per_layer(cuda_ok):
         flags[:, 2:].fill_(9)
     g.launch(comp)
     time.sleep(0.05)
-    assert not comp.query()  # parked at layer 2's waits
+    if not under_sanitizer():
+        assert not comp.query()  # parked at layer 2's waits
     deadline = time.time() + 20
     while not comp.query():
         assert time.time() < deadline, "the step never left its plane-flag waits"
