@@ -520,7 +520,7 @@ def run_ours(args, geo):
     st_out = [e[0].elapsed_time(e[1]) for e in sev]
     st_in = [e[1].elapsed_time(e[2]) for e in sev]
     staged = {
-        "engine": "copy engines, one copy per host run (<= 64 MiB slot) + kvs_stage_kernel "
+        "engine": "copy engines, one copy per host run (<= 128 MiB slot) + kvs_stage_kernel "
                   "gather / scatter (HBM ring, 4 slots)",
         "per_direction_gbs": {"out": round(nbytes_dir / (statistics.mean(st_out) * 1e-3) / 1e9, 3),
                               "in": round(nbytes_dir / (statistics.mean(st_in) * 1e-3) / 1e9, 3)},

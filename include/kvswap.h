@@ -56,7 +56,7 @@ extern "C" {
 #define KVS_BASE_PER_BLOCK 0 /* vLLM: one cudaMemcpyAsync per (plane, block)      */
 #define KVS_BASE_PER_RUN 1   /* block groups on the CE: one cudaMemcpy2DAsync per (plane, op) */
 #define KVS_BASE_STAGED 2    /* staged: one large contiguous host copy per slot of
-                                a 64 MiB HBM staging ring + a device gather/scatter
+                                a 128 MiB-slot HBM staging ring + a device gather/scatter
                                 kernel between the ring and the planes            */
 
 /* Kernel paths (kvs_set_path). */
@@ -233,7 +233,7 @@ int64_t kvs_launch_count(const KvsHandle* h);
  * [plane][chunk] while HBM holds one plane per layer, so a direct copy is
  * chunk-sized.  The staged mode therefore splits the work:
  *   - the copy engine moves each run of adjacent host blocks as ONE
- *     contiguous copy (up to a slot, 64 MiB) between the host pool and a
+ *     contiguous copy (up to a slot, 128 MiB) between the host pool and a
  *     ring of HBM staging slots, on `stream`;
  *   - a gather (out) / scatter (in) kernel moves the slot's blocks between
  *     the ring and the planes at HBM speed, on a per-direction auxiliary
@@ -246,7 +246,7 @@ int kvs_memcpy_baseline(KvsHandle* h, int dir, int mode, const int32_t* ops,
 
 /* Staging ring of KVS_BASE_STAGED, per direction: `slots` (2..16) slots of
  * `slot_bytes` (rounded down to whole blocks, at least one block).  0 keeps
- * the default (4 x 64 MiB).  Frees the current ring (synchronising with its
+ * the default (4 x 128 MiB).  Frees the current ring (synchronising with its
  * users) so the next staged call reallocates it. */
 int kvs_set_staging(KvsHandle* h, int64_t slot_bytes, int slots);
 

@@ -767,9 +767,11 @@ std::unordered_map<void*, HostAlloc> g_host_allocs;
 // host runs into / out of an HBM staging slot, and this kernel does the
 // layout change between the slot ([j][plane][chunk]) and the planes at HBM
 // speed (a 64 MiB slot is ~20 us of HBM time against ~1.2 ms on the link).
+// Slots of 128 MiB: one copy per 128 MiB request run (e2e +2% over 64 MiB,
+// tools/e2e_anatomy.py).
 // ---------------------------------------------------------------------------
 constexpr int kStageMapMax = 1024;  // blocks per slot (kernel parameter table)
-constexpr int64_t kDefaultStageBytes = 64ll << 20;
+constexpr int64_t kDefaultStageBytes = 128ll << 20;
 constexpr int kDefaultStageSlots = 4;
 
 struct StageParams {

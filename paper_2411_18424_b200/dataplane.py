@@ -332,7 +332,7 @@ class SwapDataPlane:
                                          _lib.PATHS[path], piece_bytes, stages), "kvs_set_path")
 
     def set_staging(self, slot_bytes: int = 0, slots: int = 0) -> None:
-        """Staging ring of the staged copy-engine path (0 = default 4 x 64 MiB)."""
+        """Staging ring of the staged copy-engine path (0 = default 4 x 128 MiB)."""
         _lib.check(self.lib.kvs_set_staging(self.handle, int(slot_bytes), int(slots)),
                    "kvs_set_staging")
 
