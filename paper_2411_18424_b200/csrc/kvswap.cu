@@ -138,6 +138,15 @@ __device__ __forceinline__ void publish(uint32_t* flag, uint32_t seq) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
 }
 
+// Several completion words after ONE fence: fence.acq_rel.sys followed by
+// strong (relaxed, system-scope) stores is a release pattern for each of
+// them.  A fence per word (publish) serialised ~1-2 us each in the one
+// thread that completes a plane group or a plan: 32 planes or n ops of tail
+// on every short plan (profiles/r02_layer_group_size_probe.json).
+__device__ __forceinline__ void put_after_fence(uint32_t* flag, uint32_t seq) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(seq) : "memory");
+}
+
 // Add `n` finished (and fenced) pieces of plane group `grp` to the group's
 // counter; the caller that completes the group publishes seq for every plane
 // of it.  One thread.
@@ -152,7 +161,8 @@ __device__ __forceinline__ void credit_group_1(const SwapParams<CAP>& p, uint32_
     // Every piece of the group is counted: publish, and leave the counter
     // at zero for the next launch of this direction (no memset node).
     p.plane_ctr[grp] = 0;
-    for (uint32_t l = 0; l < g_here; ++l) publish(p.plane_flags + first + l, p.seq);
+    fence_sys();  // acquire the group's counter, release to the flags' readers
+    for (uint32_t l = 0; l < g_here; ++l) put_after_fence(p.plane_flags + first + l, p.seq);
   }
 }
 
@@ -338,11 +348,11 @@ __global__ void __launch_bounds__(kMaxThreads)
       const unsigned long long t = atomicAdd(p.ticket, 1ull);
       if (t == p.ticket_base + gridDim.x - 1) {
         __threadfence_system();
+        // the fence above releases every store of the plan: one fence, then
+        // the words
         if (ops_at_end)
-          for (int32_t i = 0; i < p.n_ops; ++i) publish(p.op_flags + i, p.seq);
-        if (p.done_flag != nullptr)
-          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.seq)
-                       : "memory");
+          for (int32_t i = 0; i < p.n_ops; ++i) put_after_fence(p.op_flags + i, p.seq);
+        if (p.done_flag != nullptr) put_after_fence(p.done_flag, p.seq);
       }
     }
   }
@@ -537,11 +547,11 @@ __global__ void __launch_bounds__(32) kvs_swap_bulk_kernel(const __grid_constant
       const unsigned long long t = atomicAdd(p.ticket, 1ull);
       if (t == p.ticket_base + gridDim.x - 1) {
         __threadfence_system();
+        // the fence above releases every store of the plan: one fence, then
+        // the words
         if (ops_at_end)
-          for (int32_t i = 0; i < p.n_ops; ++i) publish(p.op_flags + i, p.seq);
-        if (p.done_flag != nullptr)
-          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.done_flag), "r"(p.seq)
-                       : "memory");
+          for (int32_t i = 0; i < p.n_ops; ++i) put_after_fence(p.op_flags + i, p.seq);
+        if (p.done_flag != nullptr) put_after_fence(p.done_flag, p.seq);
       }
     }
   }
